@@ -1,0 +1,212 @@
+/*
+ * fate.h -- C ABI of the B200-native FATE candidate scorer.
+ *
+ * Drop-in boundary for the reference's cost-matrix construction
+ *   wfsched.planner.build_problem            (pkg/src/wfsched/planner.py:75-98)
+ * and the scorer methods it calls
+ *   wfsched.costs.CostModel.plan_score       (pkg/src/wfsched/costs.py:233-247)
+ *   CostModel.sched_score / score_terms      (costs.py:149-231)
+ *   CostModel._marginal_shard_score          (costs.py:249-279)
+ *   CostModel.tail_value                     (costs.py:281-352)
+ *   CostModel.realized_duration (full batch) (costs.py:383-416, consumed by
+ *                                             FatePolicy._extend_work_conserving,
+ *                                             policies.py:91-95)
+ *
+ * Plain C: pointers and sizes only, no torch types.  Every array pointer in
+ * fate_bank / fate_state / fate_work / fate_windows / fate_derived / fate_out
+ * is a DEVICE pointer (caller-owned, e.g. torch tensors) unless the function
+ * says "host".  All launches are stream-ordered on the stream passed in
+ * (cudaStream_t cast to void*; NULL = legacy default stream).
+ *
+ * Indexing conventions (SURVEY.md §7.1 rule 2):
+ *   - stage index  = rank of the stage id in sorted(stage_ids) of its
+ *                    instance, offset by fate_bank.inst_stage_off[inst]
+ *                    ("global stage index");
+ *   - device index = rank of the device id in sorted(device_ids);
+ *   so every sorted(...) iteration of the reference is ascending-index order.
+ *
+ * Status codes: 0 = ok, < 0 = invalid argument (FATE_E*), > 0 = cudaError_t.
+ * fate_last_error() returns a thread-local message for the last failure.
+ * Arithmetic: IEEE fp64, the reference's association order, no FMA
+ * contraction; results are bit-identical to CPython 3.12 running the
+ * reference (whose builtin sum() is Neumaier-compensated).
+ */
+#ifndef FATE_H
+#define FATE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FATE_ABI_VERSION 1
+#define FATE_MAX_DEVICES 64
+#define FATE_MAX_HORIZON 32
+#define FATE_MAX_QUERIES 256
+#define FATE_MAX_KAPPA 64
+
+/* fate_weights.ablation bits (reference config.py:91-113) */
+#define FATE_NO_FUTURE_PLANNING 1u
+#define FATE_NO_LOCALITY 2u
+#define FATE_NO_SAME_MODEL 4u
+#define FATE_NO_PREFIX 8u
+#define FATE_NO_SHARD 16u
+
+/* fate_bank.st_flags bits */
+#define FATE_STAGE_CACHE_REUSE 1
+#define FATE_STAGE_KEEP_CACHE 2
+
+#define FATE_EINVAL (-1)
+#define FATE_ETOOBIG (-2)
+#define FATE_ENOTREADY (-3)
+
+/* ScoreWeights (reference config.py:116-158) as a POD constant bank.  Host
+ * memory; passed by value into the kernels' constant parameter space. */
+typedef struct fate_weights {
+    double lambda_q, lambda_s, lambda_tr, lambda_c, lambda_p, lambda_r;
+    double gamma, kappa_prefix, locality_coeff, shard_overhead_frac, demand_coeff;
+    double state_scale, locality_scale, prefix_scale, switch_x, transfer_x, prefix_x;
+    /* gamma ** l for l = 0..FATE_MAX_HORIZON-1, computed on the host with
+     * Python float pow (costs.py:349) */
+    double gamma_pow[FATE_MAX_HORIZON];
+    int32_t horizon;      /* raw weights.horizon (FatePolicy tests == 0) */
+    int32_t eff_horizon;  /* weights.effective_horizon() */
+    uint32_t ablation;    /* FATE_NO_* bits */
+    int32_t reserved;
+} fate_weights;
+
+/* Static side: one RunConfig (devices, model catalog, role table) plus a
+ * batch of workflow instances concatenated.  Device pointers. */
+typedef struct fate_bank {
+    int32_t n_devices;     /* D <= FATE_MAX_DEVICES */
+    int32_t n_models;      /* catalog models; model ids >= n_models have no profile */
+    int32_t n_roles;       /* role table rows (the neutral role included) */
+    int32_t has_overrides; /* any DeviceTopology.transfer_overrides entry */
+    int32_t n_instances;
+    int32_t n_stages;      /* total over instances */
+    int32_t n_edges;       /* total over instances */
+    int32_t n_queries;     /* total over instances */
+    int32_t max_queries;   /* max batch size over instances <= FATE_MAX_QUERIES */
+    int32_t reserved;
+    double beta_default;            /* DeviceTopology.default_transfer_coeff */
+    const double* dev_speed;        /* [D] speed_factor */
+    const int32_t* dev_topo_order;  /* [D] device index at topology position i */
+    const double* beta;             /* [D*D] transfer_coeff(src,dst), src-major */
+    const double* model_prefill;    /* [n_models] prefill_coeff */
+    const double* model_decode;     /* [n_models] decode_coeff */
+    const double* model_switch;     /* [n_models] switch_penalty */
+    const double* role_cplx;        /* [n_roles] complexity */
+    const double* role_prefill;     /* [n_roles] prefill_scale */
+    const double* role_decode;      /* [n_roles] decode_scale */
+    const double* role_comm;        /* [n_roles] comm_weight */
+    const int32_t* inst_stage_off;  /* [I] */
+    const int32_t* inst_n_stages;   /* [I] */
+    const int32_t* inst_query_off;  /* [I] */
+    const int32_t* inst_n_queries;  /* [I] */
+    /* per stage [n_stages] */
+    const int32_t* st_inst;
+    const int32_t* st_model;        /* model id, -1 = None */
+    const int32_t* st_role;         /* role row */
+    const int32_t* st_prompt;       /* prompt_token_proxy */
+    const int32_t* st_out;          /* output_token_proxy */
+    const int32_t* st_group;        /* shared_prefix_group id, -1 = None */
+    const int32_t* st_flags;        /* FATE_STAGE_* */
+    const int32_t* st_shard;        /* shard_bound R(v) */
+    const int32_t* st_level;        /* annotations.level */
+    const int32_t* st_override;     /* row into override_cost, -1 = none */
+    const uint64_t* st_elig;        /* eligible-device bitmask */
+    /* CSR adjacency over global stage indices, rows sorted ascending */
+    const int32_t* par_ptr;         /* [n_stages+1] */
+    const int32_t* par_idx;         /* [n_edges] */
+    const int32_t* ch_ptr;          /* [n_stages+1] */
+    const int32_t* ch_idx;          /* [n_edges] */
+    const double* override_cost;    /* [rows*D] base_cost_override values */
+    const uint64_t* override_mask;  /* [rows] devices present in the override */
+    /* queries [n_queries], instance order */
+    const int32_t* q_prompt;
+    const int32_t* q_group;         /* prefix group id, -1 = None */
+} fate_bank;
+
+/* Per-scenario execution-state snapshot (reference state.py:45-57 read side). */
+typedef struct fate_state {
+    int32_t n_scenarios;
+    int32_t kappa_cap;              /* prefix entries per device <= FATE_MAX_KAPPA */
+    const int32_t* scen_inst;       /* [S] instance of the scenario */
+    const double* scen_clock;       /* [S] */
+    const int64_t* scen_loc_off;    /* [S] offset of the instance-local loc row */
+    const int32_t* loc;             /* output_device(u) as device index, -1 = None */
+    const int32_t* residency;       /* [S*D] model id, -1 = None */
+    const double* dev_free;         /* [S*D] device_free */
+    const int32_t* kappa_n;         /* [S*D] live prefix entries */
+    const int32_t* kappa;           /* [S*D*cap*4] (group, tokens, model, 0) */
+} fate_state;
+
+/* Work list: one item = (scenario, stage) = one CTA-sized unit. */
+typedef struct fate_work {
+    int32_t n_items;
+    int32_t reserved;
+    const int32_t* scen;            /* [W] */
+    const int32_t* stage;           /* [W] global stage index */
+    const int64_t* psi_off;         /* [W] first psi entry of the item */
+} fate_work;
+
+/* Horizon windows: descendants of each stage bucketed by level offset
+ * l = 1..levels (levels = eff_horizon-1), each bucket ascending
+ * (reference costs.py:354-379). */
+typedef struct fate_windows {
+    int32_t levels;
+    int32_t reserved;
+    const int64_t* ptr;             /* [n_stages*levels+1] */
+    const int32_t* idx;             /* [ptr[end]] global stage indices */
+} fate_windows;
+
+/* Static per-(bank, weights) tables produced by fate_prepare. */
+typedef struct fate_derived {
+    double* mean_base;              /* [n_stages] CostModel._mean_base */
+    double* demand;                 /* [n_stages*levels] max mean_base per bucket */
+    double* split_penalty;          /* [n_stages] slot>=1 split penalty */
+    double* edge_sigma;             /* [n_edges] sigma(par_idx[e] -> child) */
+    double* edge_term;              /* [n_edges] tail locality term at beta_default */
+} fate_derived;
+
+/* Outputs.  psi: per item bound(v)*D entries, slot-major, NaN where the
+ * device is not eligible; bound(v) = 1 if no_shard else min(R(v), |A(v)|).
+ * sched/tail/completion: [W*D], NaN where not eligible; may be NULL. */
+typedef struct fate_out {
+    double* psi;
+    double* sched;
+    double* tail;
+    double* completion;
+} fate_out;
+
+int fate_abi_version(void);
+const char* fate_last_error(void);
+
+/* Host: count then fill the horizon windows from HOST CSR children +
+ * levels.  ptr_out has n_stages*levels+1 entries; idx_out has *n_items. */
+int fate_windows_count_host(int32_t n_stages, const int32_t* ch_ptr, const int32_t* ch_idx,
+                            const int32_t* level, int32_t levels, int64_t* n_items);
+int fate_windows_build_host(int32_t n_stages, const int32_t* ch_ptr, const int32_t* ch_idx,
+                            const int32_t* level, int32_t levels, int64_t* ptr_out,
+                            int32_t* idx_out);
+
+/* Device: static prologue (mean_base, demand, split penalty, edge sigma and
+ * locality terms).  Once per (bank, weights). */
+int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+                 const fate_derived* out, void* stream);
+
+/* Device: score every work item.  Ψ for all slots and eligible devices, plus
+ * the optional S / tail / completion matrices. */
+int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+               const fate_derived* der, const fate_state* st, const fate_work* work,
+               const fate_out* out, void* stream);
+
+/* Device: count kernel launches issued by this library since load (for the
+ * benchmark's gpu_launches evidence). */
+int64_t fate_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FATE_H */

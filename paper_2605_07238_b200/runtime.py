@@ -1,0 +1,222 @@
+"""Device runtime: loads ``libfate.so`` (the sm_100a kernels behind the C ABI of
+``include/fate.h``) and drives it with PyTorch-owned device buffers.
+
+There is no CPU fallback: if the library is missing, or CUDA is unavailable,
+every entry point raises :class:`FateUnavailable`.  PyTorch is plumbing only
+(device memory, streams, pinned host buffers); all scoring arithmetic runs in
+the library's kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+from .pack import PackedBank, PackedStates, WorkList, weights_record
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfate.so")
+
+
+class FateUnavailable(RuntimeError):
+    """The CUDA scorer cannot run here (library not built, or no GPU)."""
+
+
+class FateError(RuntimeError):
+    """A C-ABI call returned a nonzero status."""
+
+
+_lib = None
+
+
+def load_library():
+    """Load ``libfate.so`` (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise FateUnavailable(
+            f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    L.fate_abi_version.restype = C.c_int
+    L.fate_last_error.restype = C.c_char_p
+    L.fate_launch_count.restype = C.c_int64
+    L.fate_windows_count_host.restype = C.c_int
+    L.fate_windows_count_host.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_int32, C.POINTER(C.c_int64)]
+    L.fate_windows_build_host.restype = C.c_int
+    L.fate_windows_build_host.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_int32, C.c_void_p, C.c_void_p]
+    L.fate_prepare.restype = C.c_int
+    L.fate_prepare.argtypes = [C.c_void_p] * 5
+    L.fate_score.restype = C.c_int
+    L.fate_score.argtypes = [C.c_void_p] * 8
+    if L.fate_abi_version() != 1:
+        raise FateUnavailable("libfate.so ABI version mismatch")
+    _lib = L
+    return L
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load_library().fate_last_error().decode(errors="replace")
+        if rc < 0:
+            raise ValueError(f"{what}: {msg} (status {rc})")
+        raise FateError(f"{what}: {msg} (cuda error {rc})")
+
+
+def launch_count() -> int:
+    return int(load_library().fate_launch_count())
+
+
+def build_windows(packed: PackedBank, levels: int):
+    """Horizon-window CSR via the native host builder (cached on the bank)."""
+    if levels in packed.windows:
+        return packed.windows[levels]
+    L = load_library()
+    a = packed.arrays
+    n = packed.n_stages
+    ch_ptr = np.ascontiguousarray(a["ch_ptr"])
+    ch_idx = np.ascontiguousarray(a["ch_idx"])
+    level = np.ascontiguousarray(a["st_level"])
+    cnt = C.c_int64(0)
+    _check(L.fate_windows_count_host(n, ch_ptr.ctypes.data, ch_idx.ctypes.data,
+                                     level.ctypes.data, levels, C.byref(cnt)), "windows_count")
+    ptr = np.zeros(n * levels + 1, dtype=np.int64)
+    idx = np.zeros(max(cnt.value, 1), dtype=np.int32)
+    _check(L.fate_windows_build_host(n, ch_ptr.ctypes.data, ch_idx.ctypes.data,
+                                     level.ctypes.data, levels, ptr.ctypes.data,
+                                     idx.ctypes.data), "windows_build")
+    packed.windows[levels] = (ptr, idx)
+    return ptr, idx
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise FateUnavailable("CUDA is not available: the FATE scorer has no CPU path")
+    return torch
+
+
+def _to_dev(torch, arr: np.ndarray, device):
+    arr = np.ascontiguousarray(arr)
+    if arr.dtype == np.uint64:
+        arr = arr.view(np.int64)
+    return torch.from_numpy(arr).to(device)
+
+
+@dataclass
+class ScoreResult:
+    psi: object          # torch float64 [n_psi]
+    sched: object        # torch float64 [W*D] or None
+    tail: object
+    completion: object
+
+
+class DeviceBank:
+    """Static SoA resident in HBM for one (bank, weights) pair, plus the
+    prologue tables (windows, mean_base, demand, split penalty, edge terms)."""
+
+    def __init__(self, packed: PackedBank, weights, device=None, stream=None):
+        torch = _torch()
+        L = load_library()
+        self.torch = torch
+        self.packed = packed
+        self.weights = weights
+        self.device = torch.device(device or "cuda")
+        self.wrec = weights_record(weights)
+        self.cweights = abi.make_weights(self.wrec)
+        eff = self.wrec["eff_horizon"]
+        self.levels = eff - 1 if eff > 1 else 0
+        self.no_shard = bool(self.wrec["ablation"] & 16)
+        self.t = {k: _to_dev(torch, v, self.device) for k, v in packed.arrays.items()}
+        self.cbank = abi.fill_struct(
+            abi.FateBank(),
+            {k: packed.scalars[k] for k in abi.BANK_INTS if k in packed.scalars}
+            | {"beta_default": packed.scalars["beta_default"]},
+            {k: self.t[k].data_ptr() for k in abi.BANK_PTRS})
+        ptr, idx = build_windows(packed, self.levels)
+        self.win_ptr = _to_dev(torch, ptr, self.device)
+        self.win_idx = _to_dev(torch, idx, self.device)
+        self.cwin = abi.FateWindows(levels=self.levels, ptr=self.win_ptr.data_ptr(),
+                                    idx=self.win_idx.data_ptr())
+        n, e = packed.n_stages, packed.scalars["n_edges"]
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.mean_base = torch.empty(max(n, 1), **f64)
+        self.demand = torch.empty(max(n * self.levels, 1), **f64)
+        self.split_penalty = torch.empty(max(n, 1), **f64)
+        self.edge_sigma = torch.empty(max(e, 1), **f64)
+        self.edge_term = torch.empty(max(e, 1), **f64)
+        self.cder = abi.FateDerived(mean_base=self.mean_base.data_ptr(),
+                                    demand=self.demand.data_ptr(),
+                                    split_penalty=self.split_penalty.data_ptr(),
+                                    edge_sigma=self.edge_sigma.data_ptr(),
+                                    edge_term=self.edge_term.data_ptr())
+        s = stream or torch.cuda.current_stream(self.device)
+        _check(L.fate_prepare(C.byref(self.cbank), C.byref(self.cweights), C.byref(self.cwin),
+                              C.byref(self.cder), C.c_void_p(s.cuda_stream)), "fate_prepare")
+
+    # -- per-call inputs -------------------------------------------------------
+
+    def upload_states(self, states: PackedStates, non_blocking: bool = False) -> "DeviceStates":
+        return DeviceStates(self, states, non_blocking=non_blocking)
+
+    def upload_work(self, work: WorkList, non_blocking: bool = False) -> "DeviceWork":
+        return DeviceWork(self, work, non_blocking=non_blocking)
+
+    def alloc_out(self, work: WorkList, extras: bool = True) -> ScoreResult:
+        torch = self.torch
+        n_dev = self.packed.scalars["n_devices"]
+        f64 = dict(dtype=torch.float64, device=self.device)
+        psi = torch.empty(max(work.n_psi, 1), **f64)
+        mk = (lambda: torch.empty(max(work.n_items * n_dev, 1), **f64)) if extras else (lambda: None)
+        return ScoreResult(psi=psi, sched=mk(), tail=mk(), completion=mk())
+
+    def score_into(self, dstates: "DeviceStates", dwork: "DeviceWork", out: ScoreResult,
+                   stream=None) -> ScoreResult:
+        torch = self.torch
+        s = stream or torch.cuda.current_stream(self.device)
+        cout = abi.FateOut(
+            psi=out.psi.data_ptr(),
+            sched=out.sched.data_ptr() if out.sched is not None else None,
+            tail=out.tail.data_ptr() if out.tail is not None else None,
+            completion=out.completion.data_ptr() if out.completion is not None else None)
+        _check(load_library().fate_score(
+            C.byref(self.cbank), C.byref(self.cweights), C.byref(self.cwin), C.byref(self.cder),
+            C.byref(dstates.cstate), C.byref(dwork.cwork), C.byref(cout),
+            C.c_void_p(s.cuda_stream)), "fate_score")
+        return out
+
+    def score(self, states: PackedStates, work: WorkList, extras: bool = True) -> ScoreResult:
+        ds = self.upload_states(states)
+        dw = self.upload_work(work)
+        out = self.alloc_out(work, extras)
+        return self.score_into(ds, dw, out)
+
+
+class DeviceStates:
+    def __init__(self, dbank: DeviceBank, states: PackedStates, non_blocking: bool = False):
+        torch = dbank.torch
+        self.states = states
+        self.t = {}
+        for k, v in states.arrays.items():
+            src = torch.from_numpy(np.ascontiguousarray(v))
+            self.t[k] = src.to(dbank.device, non_blocking=non_blocking)
+        self.cstate = abi.fill_struct(
+            abi.FateState(), {"n_scenarios": states.n_scenarios, "kappa_cap": states.kappa_cap},
+            {k: self.t[k].data_ptr() for k in abi.STATE_PTRS})
+
+
+class DeviceWork:
+    def __init__(self, dbank: DeviceBank, work: WorkList, non_blocking: bool = False):
+        torch = dbank.torch
+        self.work = work
+        self.t = {k: torch.from_numpy(np.ascontiguousarray(getattr(work, k))).to(
+            dbank.device, non_blocking=non_blocking) for k in ("scen", "stage", "psi_off")}
+        self.cwork = abi.fill_struct(abi.FateWork(), {"n_items": work.n_items},
+                                     {k: v.data_ptr() for k, v in self.t.items()})

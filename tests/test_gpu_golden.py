@@ -1,0 +1,71 @@
+"""GPU path vs golden vectors captured from the REFERENCE (end to end).
+
+For configs 1-3 the mirror executor runs the FATE policy with the GPU scorer;
+every wave's Psi / S / completion must equal the reference's bits and the final
+RunRecord (makespan, p95, counters, per-query completions) must be identical.
+Config 2 additionally reproduces table1's FATE row (normalised makespan/P95 vs
+RoundRobin, mechanism rates) from the replayed FATE records and the golden
+baseline records.  Configs 4/5: sampled Psi/S/tail/completion on the canonical
+scenario states.
+"""
+
+from __future__ import annotations
+
+import pytest
+
+from paper_2605_07238_b200.planner import GpuScorer
+
+import golden_replay as G
+import golden_checks as GC
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def scorer():
+    return GpuScorer()
+
+
+def test_c1_all_variants(scorer):
+    runs, arrs = G.load("c1")
+    bad = {}
+    for r in runs:
+        inst, cfg = G.c1_setup(r["variant"])
+        _, problems, _ = G.replay(r, arrs, inst, cfg, scorer)
+        if problems:
+            bad[r["variant"]["tag"]] = problems[:3]
+    assert not bad, bad
+
+
+def test_c1_known_answer(scorer):
+    GC.check_c1_known_answer(scorer)
+
+
+def test_c3_prefix_suite(scorer):
+    runs, arrs = G.load("c3")
+    bad = []
+    for r in runs:
+        inst, cfg = G.c3_setup(r["ratio"], r["batch"], r["shape"])
+        _, problems, _ = G.replay(r, arrs, inst, cfg, scorer)
+        if problems:
+            bad.append(((r["ratio"], r["batch"], r["shape"]), problems[:3]))
+    assert not bad, bad
+    GC.check_c3_table(runs)
+
+
+def test_c2_suite_and_table1(scorer):
+    runs, arrs = G.load("c2")
+    bad = []
+    records = []
+    for r in runs:
+        inst, cfg = G.c2_setup(r["key"])
+        rec, problems, _ = G.replay(r, arrs, inst, cfg, scorer)
+        records.append(rec)
+        if problems:
+            bad.append((r["key"], problems[:3]))
+    assert not bad, bad[:5]
+    GC.check_c2_table1(records)
+
+
+def test_c45_sampled(scorer):
+    GC.check_c45_sampled(gpu=True)
