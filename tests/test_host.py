@@ -1,0 +1,172 @@
+"""CPU tests of the host side: C-ABI library exports, native window builder,
+packer invariants, solver vs exhaustive enumeration (no GPU needed)."""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+from paper_2605_07238_b200 import pack, runtime, scenarios
+from paper_2605_07238_b200.wf.frontier import (
+    Candidate, FrontierProblem, check_constraints, solve_frontier,
+)
+
+from cases import c5_case, edge_case, small_case
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    text = open(os.path.join(ROOT, "include", "fate.h")).read()
+    return re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(fate_\w+)\s*\(", text, re.M)
+
+
+def test_library_exports_every_declared_symbol():
+    if not os.path.exists(runtime.LIB_PATH):
+        pytest.skip("libfate.so not built")
+    lib = ctypes.CDLL(runtime.LIB_PATH)
+    names = _declared_functions()
+    assert {"fate_score", "fate_prepare", "fate_windows_build_host"} <= set(names)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert runtime.load_library().fate_abi_version() == 1
+
+
+def _py_windows(bank, levels):
+    a = bank.arrays
+    ptr = [0]
+    idx = []
+    lvl = a["st_level"]
+    ch_ptr, ch_idx = a["ch_ptr"], a["ch_idx"]
+    for v in range(bank.n_stages):
+        seen, front, found = set(), [v], []
+        while front:  # full descendant walk, like the reference
+            nxt = []
+            for u in front:
+                for c in ch_idx[ch_ptr[u]:ch_ptr[u + 1]]:
+                    if c not in seen:
+                        seen.add(int(c))
+                        nxt.append(int(c))
+            front = nxt
+        for l in range(1, levels + 1):
+            bucket = sorted(x for x in seen if lvl[x] - lvl[v] == l)
+            idx += bucket
+            ptr.append(len(idx))
+    return np.asarray(ptr), np.asarray(idx)
+
+
+@pytest.mark.parametrize("levels", [0, 1, 2, 3, 5])
+def test_native_windows_equal_full_descendant_walk(levels):
+    if not os.path.exists(runtime.LIB_PATH):
+        pytest.skip("libfate.so not built")
+    for case in (edge_case(), small_case(), c5_case(n_inst=2)):
+        bank = case.bank
+        bank.windows.clear()
+        ptr, idx = runtime.build_windows(bank, levels)
+        want_ptr, want_idx = _py_windows(bank, levels)
+        assert np.array_equal(ptr, want_ptr)
+        assert np.array_equal(idx[: ptr[-1]], want_idx)
+
+
+def test_pack_roundtrip_state():
+    case = edge_case()
+    bank = case.bank
+    st = case.states
+    D = bank.scalars["n_devices"]
+    # residency / free / kappa round trip for scenario 0
+    import cases as C
+
+    c = C.edge_case()
+    assert np.array_equal(c.states.arrays["residency"], st.arrays["residency"])
+    assert st.kappa_cap >= 1
+    assert st.arrays["residency"].size == st.n_scenarios * D
+
+
+def test_bounds_follow_planner_rule():
+    case = edge_case(horizon=2)
+    for w in range(case.work.n_items):
+        g = int(case.work.stage[w])
+        R = int(case.bank.arrays["st_shard"][g])
+        n = bin(int(case.bank.arrays["st_elig"][g])).count("1")
+        assert case.work.bounds[w] == min(R, n)
+
+
+def _random_problem(rng, n_stages, n_dev):
+    devs = [f"d{i}" for i in range(n_dev)]
+    cands, bounds = [], {}
+    for s in range(n_stages):
+        sid = f"s{s:02d}"
+        b = rng.choice([1, 2])
+        bounds[sid] = b
+        for k in range(b):
+            for d in devs:
+                cands.append(Candidate(sid, k, d, round(rng.uniform(-10, 10), 4)))
+    return FrontierProblem(tuple(cands), bounds, tuple(devs))
+
+
+def _enumerate(problem):
+    """Exhaustive optimum (same objective and tie-break as the reference's
+    verification.enumerate_optimum, verification.py:36-71)."""
+    by = {}
+    for c in problem.candidates:
+        by.setdefault(c.stage_id, {}).setdefault(c.slot, {})[c.device_id] = c.psi
+    stages = sorted(by)
+    per = []
+    for sid in stages:
+        opts = [((), 0.0)]
+        devs = sorted(problem.device_ids)
+        for n in range(1, len(by[sid]) + 1):
+            for combo in itertools.permutations(devs, n):
+                if all(d in by[sid][k] for k, d in enumerate(combo)):
+                    val = 0.0
+                    for k, d in enumerate(combo):
+                        val += by[sid][k][d]
+                    opts.append((tuple((sid, k, d) for k, d in enumerate(combo)), val))
+        per.append(opts)
+    best = (0.0, ())
+    for choice in itertools.product(*per):
+        used = [d for t, _ in choice for (_, _, d) in t]
+        if len(used) != len(set(used)):
+            continue
+        val = 0.0
+        for _, v in choice:
+            val += v
+        sel = tuple(sorted(x for t, _ in choice for x in t))
+        if val > best[0] + 1e-12:
+            best = (val, sel)
+    return best
+
+
+def test_solver_matches_exhaustive_search():
+    rng = random.Random(7)
+    for _ in range(60):
+        prob = _random_problem(rng, rng.randint(1, 4), rng.randint(1, 3))
+        sol = solve_frontier(prob, budget_s=5.0)
+        assert sol.optimal
+        assert not check_constraints(prob, sol.selected)
+        opt, _ = _enumerate(prob)
+        assert abs(sol.objective - opt) <= 1e-9
+
+
+def test_solver_timeout_falls_back_to_greedy():
+    rng = random.Random(1)
+    prob = _random_problem(rng, 6, 4)
+    sol = solve_frontier(prob, budget_s=0.0)
+    assert not check_constraints(prob, sol.selected)
+
+
+def test_scenario_generator_is_deterministic():
+    cfg = scenarios.config_c5()
+    inst = scenarios.c5_instance(3, cfg)
+    a = scenarios.build_scenario(inst, cfg, 3)
+    b = scenarios.build_scenario(inst, cfg, 3)
+    assert a.clock == b.clock and a.residency == b.residency
+    assert a.parent_loc == b.parent_loc and a.device_free == b.device_free
+    front = scenarios.scenario_frontier(inst, a)
+    assert len(front) == 25
