@@ -322,11 +322,22 @@ __global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weigh
     }
     __syncthreads();
 
-    if (!dev_ok) return;  // no barriers below
+    if (!(live && d < D)) return;  // no barriers below
+    const int n_elig = __popcll(elig);
+    const int bound = (w.ablation & FATE_NO_SHARD) ? 1 : (R < n_elig ? R : n_elig);
+    if (!dev_ok) {
+        // ineligible device: no candidate; NaN marks the hole in the dense rows
+        const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+        double* psi = out.psi + work.psi_off[item];
+        for (int k = 0; k < bound; ++k) psi[(long long)k * D + d] = qnan;
+        const long long orow = item * D + d;
+        if (out.sched) out.sched[orow] = qnan;
+        if (out.tail) out.tail[orow] = qnan;
+        if (out.completion) out.completion[orow] = qnan;
+        return;
+    }
 
     // ---- D: per-candidate terms ------------------------------------------------
-    const double nan_v = __longlong_as_double(0x7ff8000000000000LL);
-    (void)nan_v;
     const double free_d = st.dev_free[dev_row0 + d];
     const double wait = py_max0(free_d - clock);
     const double sw = sm.swc[d];
@@ -459,16 +470,12 @@ __global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weigh
     psi[d] = S + tail;
 
     // _marginal_shard_score (costs.py:249-279), slots 1..bound-1
-    const int n_elig = __popcll(elig);
-    const int bound = no_shard ? 1 : (R < n_elig ? R : n_elig);
     if (bound > 1) {
         const double bb = sm.bb[0];
         const double hi_v = here > bb ? here : bb;
         const double overhead = w.shard_overhead_frac * bb;
         const double tr_m = no_loc ? 0.0 : tr;
         const double split = no_loc ? 0.0 : der.split_penalty[v];
-        const double common = -(w.lambda_q * wait);
-        (void)common;
         for (int k = 1; k < bound; ++k) {
             const double reduction = bb / (double)k - hi_v / (double)(k + 1);
             psi[(long long)k * D + d] = w.lambda_r * (reduction - overhead) - w.lambda_q * wait -
@@ -476,28 +483,6 @@ __global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weigh
                                         w.lambda_tr * (tr_m + split) * w.locality_scale;
         }
     }
-}
-
-// NaN-fill of ineligible entries: one thread per (item, device)
-__global__ void fate_fill_ineligible_kernel(fate_bank b, fate_weights w, fate_work work,
-                                            fate_out out) {
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int D = b.n_devices;
-    if (t >= (long long)work.n_items * D) return;
-    const long long item = t / D;
-    const int d = (int)(t - item * D);
-    const int v = work.stage[item];
-    const uint64_t elig = b.st_elig[v];
-    if ((elig >> d) & 1ull) return;
-    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
-    const int R = b.st_shard[v];
-    const int n_elig = __popcll(elig);
-    const int bound = (w.ablation & FATE_NO_SHARD) ? 1 : (R < n_elig ? R : n_elig);
-    double* psi = out.psi + work.psi_off[item];
-    for (int k = 0; k < bound; ++k) psi[(long long)k * D + d] = qnan;
-    if (out.sched) out.sched[t] = qnan;
-    if (out.tail) out.tail[t] = qnan;
-    if (out.completion) out.completion[t] = qnan;
 }
 
 int check_bank(const fate_bank* b) {
@@ -595,11 +580,7 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
                                                                *out);
     }
     g_launches++;
-    if ((rc = cuda_status("fate_score_kernel"))) return rc;
-    const long long n = (long long)work->n_items * D;
-    fate_fill_ineligible_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(*bank, *w, *work, *out);
-    g_launches++;
-    return cuda_status("fate_fill_ineligible_kernel");
+    return cuda_status("fate_score_kernel");
 }
 
 }  // extern "C"

@@ -220,3 +220,51 @@ class DeviceWork:
             dbank.device, non_blocking=non_blocking) for k in ("scen", "stage", "psi_off")}
         self.cwork = abi.fill_struct(abi.FateWork(), {"n_items": work.n_items},
                                      {k: v.data_ptr() for k, v in self.t.items()})
+
+
+class HostPipeline:
+    """Reference-facing call with HOST buffers: per call, the scenario states
+    and work list are copied host->device from pinned memory, scored, and Psi
+    copied device->host into pinned memory -- all stream-ordered on one stream
+    (the static bank is HBM-resident, uploaded once like model weights)."""
+
+    def __init__(self, dbank: DeviceBank, states: PackedStates, work: WorkList,
+                 extras: bool = False):
+        torch = dbank.torch
+        self.dbank = dbank
+        self.host_in = {}
+        for k, v in states.arrays.items():
+            self.host_in["s:" + k] = torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+        for k in ("scen", "stage", "psi_off"):
+            self.host_in["w:" + k] = torch.from_numpy(
+                np.ascontiguousarray(getattr(work, k))).pin_memory()
+        self.dev_in = {k: torch.empty_like(v, device=dbank.device) for k, v in self.host_in.items()}
+        self.cstate = abi.fill_struct(
+            abi.FateState(), {"n_scenarios": states.n_scenarios, "kappa_cap": states.kappa_cap},
+            {k: self.dev_in["s:" + k].data_ptr() for k in abi.STATE_PTRS})
+        self.cwork = abi.fill_struct(abi.FateWork(), {"n_items": work.n_items},
+                                     {k: self.dev_in["w:" + k].data_ptr()
+                                      for k in ("scen", "stage", "psi_off")})
+        self.out = dbank.alloc_out(work, extras=extras)
+        self.host_psi = torch.empty(self.out.psi.shape, dtype=torch.float64).pin_memory()
+        self.h2d_bytes = sum(v.numel() * v.element_size() for v in self.host_in.values())
+        self.d2h_bytes = self.host_psi.numel() * 8
+
+    def run(self, stream=None):
+        torch = self.dbank.torch
+        s = stream or torch.cuda.current_stream(self.dbank.device)
+        with torch.cuda.stream(s):
+            for k, v in self.host_in.items():
+                self.dev_in[k].copy_(v, non_blocking=True)
+            cout = abi.FateOut(psi=self.out.psi.data_ptr(),
+                               sched=self.out.sched.data_ptr() if self.out.sched is not None else None,
+                               tail=self.out.tail.data_ptr() if self.out.tail is not None else None,
+                               completion=(self.out.completion.data_ptr()
+                                           if self.out.completion is not None else None))
+            d = self.dbank
+            _check(load_library().fate_score(
+                C.byref(d.cbank), C.byref(d.cweights), C.byref(d.cwin), C.byref(d.cder),
+                C.byref(self.cstate), C.byref(self.cwork), C.byref(cout),
+                C.c_void_p(s.cuda_stream)), "fate_score")
+            self.host_psi.copy_(self.out.psi, non_blocking=True)
+        return self.host_psi
