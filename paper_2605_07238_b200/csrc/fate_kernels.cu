@@ -33,6 +33,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -485,6 +486,32 @@ __global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weigh
     }
 }
 
+#include "fate_score_v2.cuh"
+
+template <int G>
+int launch_v2(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+              const fate_derived* der, const fate_state* st, const fate_work* work,
+              const fate_out* out, cudaStream_t s) {
+    constexpr int NT = 128, IPB = NT / G;
+    const size_t smem = v2_item_bytes(bank->n_devices, bank->max_queries, win->levels) * IPB;
+    if (smem > 200 * 1024) return fail(FATE_ETOOBIG, "v2 shared-memory footprint too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fate_score_v2_kernel<G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    const unsigned blocks = (unsigned)((work->n_items + IPB - 1) / IPB);
+    fate_score_v2_kernel<G, NT><<<blocks, NT, smem, s>>>(*bank, *w, *win, *der, *st, *work, *out);
+    return 0;
+}
+
+bool use_v1() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FATE_SCORE_KERNEL");
+        v = (e && strcmp(e, "v1") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 int check_bank(const fate_bank* b) {
     if (!b) return fail(FATE_EINVAL, "bank is NULL");
     if (b->n_devices < 1 || b->n_devices > FATE_MAX_DEVICES)
@@ -558,7 +585,11 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int D = bank->n_devices;
     const size_t per_item = item_smem_bytes(D, bank->max_queries);
-    if (D <= 32) {
+    if (!use_v1()) {
+        rc = D <= 32 ? launch_v2<32>(bank, w, win, der, st, work, out, s)
+                     : launch_v2<64>(bank, w, win, der, st, work, out, s);
+        if (rc) return rc;
+    } else if (D <= 32) {
         constexpr int TPI = 32, IPB = 128 / TPI;
         const size_t smem = per_item * IPB;
         if (smem > 48 * 1024) {
