@@ -156,7 +156,7 @@ typedef struct fate_work {
  * (reference costs.py:354-379). */
 typedef struct fate_windows {
     int32_t levels;
-    int32_t reserved;
+    int32_t max_level_ops;          /* max over (v,l) of sum_{x in bucket}(2+|Pa(x)|) */
     const int64_t* ptr;             /* [n_stages*levels+1] */
     const int32_t* idx;             /* [ptr[end]] global stage indices */
 } fate_windows;
@@ -168,6 +168,9 @@ typedef struct fate_derived {
     double* split_penalty;          /* [n_stages] slot>=1 split penalty */
     double* edge_sigma;             /* [n_edges] sigma(par_idx[e] -> child) */
     double* edge_term;              /* [n_edges] tail locality term at beta_default */
+    double* tail_static;            /* [n_stages*levels*(n_models+1)] affinity chain per
+                                       (stage, level, displacement class) with no locality
+                                       op applied (costs.py:307-331) */
 } fate_derived;
 
 /* Outputs.  psi: per item bound(v)*D entries, slot-major, NaN where the

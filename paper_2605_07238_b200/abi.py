@@ -58,12 +58,12 @@ class FateWork(C.Structure):
 
 
 class FateWindows(C.Structure):
-    _fields_ = [("levels", C.c_int32), ("reserved", C.c_int32), ("ptr", _p), ("idx", _p)]
+    _fields_ = [("levels", C.c_int32), ("max_level_ops", C.c_int32), ("ptr", _p), ("idx", _p)]
 
 
 class FateDerived(C.Structure):
     _fields_ = [(n, _p) for n in ("mean_base", "demand", "split_penalty", "edge_sigma",
-                                  "edge_term")]
+                                  "edge_term", "tail_static")]
 
 
 class FateOut(C.Structure):

@@ -487,6 +487,22 @@ __global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weigh
 }
 
 #include "fate_score_v2.cuh"
+#include "fate_score_v3.cuh"
+
+template <int G>
+int launch_v3(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+              const fate_derived* der, const fate_state* st, const fate_work* work,
+              const fate_out* out, cudaStream_t s) {
+    constexpr int IPB = 128 / G;
+    const size_t smem = v3_item_bytes(bank->n_devices, bank->max_queries, G, win->max_level_ops) * IPB;
+    if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v3 shared-memory footprint too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fate_score_v3_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    const unsigned blocks = (unsigned)((work->n_items + IPB - 1) / IPB);
+    fate_score_v3_kernel<G><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st, *work, *out);
+    return 0;
+}
 
 template <int G>
 int launch_v2(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
@@ -503,13 +519,14 @@ int launch_v2(const fate_bank* bank, const fate_weights* w, const fate_windows* 
     return 0;
 }
 
-bool use_v1() {
+// Kernel generation (A/B benchmarking only): FATE_SCORE_KERNEL=v1|v2, default v3.
+int kernel_gen() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FATE_SCORE_KERNEL");
-        v = (e && strcmp(e, "v1") == 0) ? 1 : 0;
+        v = (e && strcmp(e, "v1") == 0) ? 1 : (e && strcmp(e, "v2") == 0) ? 2 : 3;
     }
-    return v == 1;
+    return v;
 }
 
 int check_bank(const fate_bank* b) {
@@ -565,6 +582,13 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
                 *bank, *win, *out);
             g_launches++;
             if ((rc = cuda_status("fate_prepare_demand_kernel"))) return rc;
+            if (out->tail_static) {
+                const long long nt = n * (bank->n_models + 1);
+                fate_prepare_tail_static_kernel<<<(unsigned)((nt + threads - 1) / threads), threads, 0,
+                                                  s>>>(*bank, *w, *win, out->tail_static);
+                g_launches++;
+                if ((rc = cuda_status("fate_prepare_tail_static_kernel"))) return rc;
+            }
         }
     }
     return 0;
@@ -585,7 +609,11 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int D = bank->n_devices;
     const size_t per_item = item_smem_bytes(D, bank->max_queries);
-    if (!use_v1()) {
+    if (kernel_gen() == 3) {
+        rc = D <= 32 ? launch_v3<32>(bank, w, win, der, st, work, out, s)
+                     : launch_v3<64>(bank, w, win, der, st, work, out, s);
+        if (rc) return rc;
+    } else if (kernel_gen() == 2) {
         rc = D <= 32 ? launch_v2<32>(bank, w, win, der, st, work, out, s)
                      : launch_v2<64>(bank, w, win, der, st, work, out, s);
         if (rc) return rc;

@@ -95,6 +95,29 @@ def build_windows(packed: PackedBank, levels: int):
     return ptr, idx
 
 
+def max_level_ops(packed: PackedBank, levels: int) -> int:
+    """Largest per-(stage, level) op count of the tail: sum over the bucket of
+    (model op + prefix op + parent edges); sizes the kernel's op buffer."""
+    if levels == 0:
+        return 0
+    key = ("ops", levels)
+    if key in packed.windows:
+        return packed.windows[key]
+    ptr, idx = build_windows(packed, levels)
+    a = packed.arrays
+    npar = (a["par_ptr"][1:] - a["par_ptr"][:-1]).astype(np.int64)
+    n_items = int(ptr[-1])
+    if n_items == 0:
+        packed.windows[key] = 0
+        return 0
+    per_item = 2 + npar[idx[:n_items]]
+    csum = np.concatenate([[0], np.cumsum(per_item)])
+    per_bucket = csum[ptr[1:]] - csum[ptr[:-1]]
+    out = int(per_bucket.max()) if per_bucket.size else 0
+    packed.windows[key] = out
+    return out
+
+
 def _torch():
     import torch
 
@@ -143,8 +166,9 @@ class DeviceBank:
         ptr, idx = build_windows(packed, self.levels)
         self.win_ptr = _to_dev(torch, ptr, self.device)
         self.win_idx = _to_dev(torch, idx, self.device)
-        self.cwin = abi.FateWindows(levels=self.levels, ptr=self.win_ptr.data_ptr(),
-                                    idx=self.win_idx.data_ptr())
+        self.cwin = abi.FateWindows(levels=self.levels,
+                                    max_level_ops=max_level_ops(packed, self.levels),
+                                    ptr=self.win_ptr.data_ptr(), idx=self.win_idx.data_ptr())
         n, e = packed.n_stages, packed.scalars["n_edges"]
         f64 = dict(dtype=torch.float64, device=self.device)
         self.mean_base = torch.empty(max(n, 1), **f64)
@@ -152,11 +176,14 @@ class DeviceBank:
         self.split_penalty = torch.empty(max(n, 1), **f64)
         self.edge_sigma = torch.empty(max(e, 1), **f64)
         self.edge_term = torch.empty(max(e, 1), **f64)
+        n_static = n * self.levels * (packed.scalars["n_models"] + 1)
+        self.tail_static = torch.empty(max(n_static, 1), **f64)
         self.cder = abi.FateDerived(mean_base=self.mean_base.data_ptr(),
                                     demand=self.demand.data_ptr(),
                                     split_penalty=self.split_penalty.data_ptr(),
                                     edge_sigma=self.edge_sigma.data_ptr(),
-                                    edge_term=self.edge_term.data_ptr())
+                                    edge_term=self.edge_term.data_ptr(),
+                                    tail_static=self.tail_static.data_ptr())
         s = stream or torch.cuda.current_stream(self.device)
         _check(L.fate_prepare(C.byref(self.cbank), C.byref(self.cweights), C.byref(self.cwin),
                               C.byref(self.cder), C.c_void_p(s.cuda_stream)), "fate_prepare")
