@@ -89,6 +89,18 @@ struct PySum {
 
 __device__ __forceinline__ double py_max0(double x) { return x > 0.0 ? x : 0.0; }
 
+__device__ __forceinline__ unsigned long long low_mask(int d) {
+    return d >= 64 ? ~0ull : ((1ull << d) - 1ull);
+}
+
+// Shard i of k over nq queries (_even_split, costs.py:419-428): contiguous,
+// sizes nq/k + (i < nq%k)
+__device__ __forceinline__ void shard_range(int nq, int k, int i, int* lo, int* hi) {
+    const int base = nq / k, extra = nq % k;
+    *lo = i * base + (i < extra ? i : extra);
+    *hi = *lo + base + (i < extra ? 1 : 0);
+}
+
 // state.cached_tokens (state.py:110-123): group -1 = None, model -1 = None
 __device__ __forceinline__ int cached_tokens(const int32_t* __restrict__ kap, int n, int group,
                                              int model) {
@@ -486,8 +498,22 @@ __global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weigh
     }
 }
 
-#include "fate_score_v2.cuh"
 #include "fate_score_v3.cuh"
+#include "fate_score_v4.cuh"
+
+template <int DPL>
+int launch_v4(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+              const fate_derived* der, const fate_state* st, const fate_work* work,
+              const fate_out* out, cudaStream_t s) {
+    const size_t smem = v4_item_bytes(bank->n_devices, bank->max_queries, win->max_level_ops) * 4;
+    if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v4 shared-memory footprint too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fate_score_v4_kernel<DPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    const unsigned blocks = (unsigned)((work->n_items + 3) / 4);
+    fate_score_v4_kernel<DPL><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st, *work, *out);
+    return 0;
+}
 
 template <int G>
 int launch_v3(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
@@ -504,27 +530,12 @@ int launch_v3(const fate_bank* bank, const fate_weights* w, const fate_windows* 
     return 0;
 }
 
-template <int G>
-int launch_v2(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
-              const fate_derived* der, const fate_state* st, const fate_work* work,
-              const fate_out* out, cudaStream_t s) {
-    constexpr int NT = 128, IPB = NT / G;
-    const size_t smem = v2_item_bytes(bank->n_devices, bank->max_queries, win->levels) * IPB;
-    if (smem > 200 * 1024) return fail(FATE_ETOOBIG, "v2 shared-memory footprint too large");
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fate_score_v2_kernel<G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    const unsigned blocks = (unsigned)((work->n_items + IPB - 1) / IPB);
-    fate_score_v2_kernel<G, NT><<<blocks, NT, smem, s>>>(*bank, *w, *win, *der, *st, *work, *out);
-    return 0;
-}
-
-// Kernel generation (A/B benchmarking only): FATE_SCORE_KERNEL=v1|v2, default v3.
+// Kernel generation (A/B benchmarking only): FATE_SCORE_KERNEL=v1|v3, default v4.
 int kernel_gen() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FATE_SCORE_KERNEL");
-        v = (e && strcmp(e, "v1") == 0) ? 1 : (e && strcmp(e, "v2") == 0) ? 2 : 3;
+        v = (e && strcmp(e, "v1") == 0) ? 1 : (e && strcmp(e, "v3") == 0) ? 3 : 4;
     }
     return v;
 }
@@ -609,13 +620,13 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int D = bank->n_devices;
     const size_t per_item = item_smem_bytes(D, bank->max_queries);
-    if (kernel_gen() == 3) {
+    if (kernel_gen() == 4) {
+        rc = D <= 32 ? launch_v4<1>(bank, w, win, der, st, work, out, s)
+                     : launch_v4<2>(bank, w, win, der, st, work, out, s);
+        if (rc) return rc;
+    } else if (kernel_gen() == 3) {
         rc = D <= 32 ? launch_v3<32>(bank, w, win, der, st, work, out, s)
                      : launch_v3<64>(bank, w, win, der, st, work, out, s);
-        if (rc) return rc;
-    } else if (kernel_gen() == 2) {
-        rc = D <= 32 ? launch_v2<32>(bank, w, win, der, st, work, out, s)
-                     : launch_v2<64>(bank, w, win, der, st, work, out, s);
         if (rc) return rc;
     } else if (D <= 32) {
         constexpr int TPI = 32, IPB = 128 / TPI;
