@@ -53,6 +53,9 @@ extern "C" {
 #define FATE_NO_PREFIX 8u
 #define FATE_NO_SHARD 16u
 
+/* fate_bank.flags bits */
+#define FATE_BANK_UNIFORM_SPEED 1   /* every device has the same speed_factor */
+
 /* fate_bank.st_flags bits */
 #define FATE_STAGE_CACHE_REUSE 1
 #define FATE_STAGE_KEEP_CACHE 2
@@ -88,7 +91,7 @@ typedef struct fate_bank {
     int32_t n_edges;       /* total over instances */
     int32_t n_queries;     /* total over instances */
     int32_t max_queries;   /* max batch size over instances <= FATE_MAX_QUERIES */
-    int32_t reserved;
+    int32_t flags;         /* FATE_BANK_* */
     double beta_default;            /* DeviceTopology.default_transfer_coeff */
     const double* dev_speed;        /* [D] speed_factor */
     const int32_t* dev_topo_order;  /* [D] device index at topology position i */
@@ -159,6 +162,8 @@ typedef struct fate_windows {
     int32_t max_level_ops;          /* max over (v,l) of sum_{x in bucket}(2+|Pa(x)|) */
     const int64_t* ptr;             /* [n_stages*levels+1] */
     const int32_t* idx;             /* [ptr[end]] global stage indices */
+    const int64_t* wpar_ptr;        /* [n_stages*levels+1] window parents per (v, l) */
+    const int32_t* wpar_idx;        /* distinct parents != v of the bucket, ascending */
 } fate_windows;
 
 /* Static per-(bank, weights) tables produced by fate_prepare. */
@@ -168,6 +173,9 @@ typedef struct fate_derived {
     double* split_penalty;          /* [n_stages] slot>=1 split penalty */
     double* edge_sigma;             /* [n_edges] sigma(par_idx[e] -> child) */
     double* edge_term;              /* [n_edges] tail locality term at beta_default */
+    double* row0_sums;              /* [n_stages*3] stateless-row Neumaier sums: full batch,
+                                       k=2 shards 0 and 1 (valid when bank flags has
+                                       FATE_BANK_UNIFORM_SPEED) */
     double* tail_static;            /* [n_stages*levels*(n_models+1)] affinity chain per
                                        (stage, level, displacement class) with no locality
                                        op applied (costs.py:307-331) */
@@ -193,6 +201,13 @@ int fate_windows_count_host(int32_t n_stages, const int32_t* ch_ptr, const int32
 int fate_windows_build_host(int32_t n_stages, const int32_t* ch_ptr, const int32_t* ch_idx,
                             const int32_t* level, int32_t levels, int64_t* ptr_out,
                             int32_t* idx_out);
+
+/* Host: distinct window parents per (v, l); call with NULL outputs to count
+ * (*n_out), then with ptr_out [n_stages*levels+1] and idx_out [*n_out]. */
+int fate_window_parents_host(int32_t n_stages, int32_t levels, const int64_t* win_ptr,
+                             const int32_t* win_idx, const int32_t* par_ptr,
+                             const int32_t* par_idx, int64_t* ptr_out, int32_t* idx_out,
+                             int64_t* n_out);
 
 /* Device: static prologue (mean_base, demand, split penalty, edge sigma and
  * locality terms).  Once per (bank, weights). */

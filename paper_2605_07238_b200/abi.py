@@ -30,7 +30,7 @@ class FateWeights(C.Structure):
 
 
 BANK_INTS = ("n_devices", "n_models", "n_roles", "has_overrides", "n_instances", "n_stages",
-             "n_edges", "n_queries", "max_queries", "reserved")
+             "n_edges", "n_queries", "max_queries", "flags")
 BANK_PTRS = ("dev_speed", "dev_topo_order", "beta", "model_prefill", "model_decode",
              "model_switch", "role_cplx", "role_prefill", "role_decode", "role_comm",
              "inst_stage_off", "inst_n_stages", "inst_query_off", "inst_n_queries",
@@ -58,12 +58,13 @@ class FateWork(C.Structure):
 
 
 class FateWindows(C.Structure):
-    _fields_ = [("levels", C.c_int32), ("max_level_ops", C.c_int32), ("ptr", _p), ("idx", _p)]
+    _fields_ = [("levels", C.c_int32), ("max_level_ops", C.c_int32), ("ptr", _p), ("idx", _p),
+                ("wpar_ptr", _p), ("wpar_idx", _p)]
 
 
 class FateDerived(C.Structure):
     _fields_ = [(n, _p) for n in ("mean_base", "demand", "split_penalty", "edge_sigma",
-                                  "edge_term", "tail_static")]
+                                  "edge_term", "row0_sums", "tail_static")]
 
 
 class FateOut(C.Structure):

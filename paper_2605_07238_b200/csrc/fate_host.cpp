@@ -88,4 +88,41 @@ int fate_windows_build_host(int32_t n_stages, const int32_t* ch_ptr, const int32
     return 0;
 }
 
+// Window parents: per (stage v, level l) the distinct parents p != v of the
+// bucket's descendants, ascending -- the stages whose output location decides
+// whether the level's tail chain has any locality op (costs.py:332-348).
+static void wpar_of(int64_t vl, int32_t v, const int64_t* win_ptr, const int32_t* win_idx,
+                    const int32_t* par_ptr, const int32_t* par_idx, std::vector<int32_t>& out) {
+    out.clear();
+    for (int64_t i = win_ptr[vl]; i < win_ptr[vl + 1]; ++i) {
+        const int32_t x = win_idx[i];
+        for (int32_t e = par_ptr[x]; e < par_ptr[x + 1]; ++e)
+            if (par_idx[e] != v) out.push_back(par_idx[e]);
+    }
+    std::sort(out.begin(), out.end());
+    out.erase(std::unique(out.begin(), out.end()), out.end());
+}
+
+int fate_window_parents_host(int32_t n_stages, int32_t levels, const int64_t* win_ptr,
+                             const int32_t* win_idx, const int32_t* par_ptr,
+                             const int32_t* par_idx, int64_t* ptr_out, int32_t* idx_out,
+                             int64_t* n_out) {
+    if (n_stages < 0 || levels < 0 || !n_out) return FATE_EINVAL;
+    std::vector<int32_t> buf;
+    int64_t pos = 0;
+    if (ptr_out) ptr_out[0] = 0;
+    for (int32_t v = 0; v < n_stages; ++v) {
+        for (int32_t l = 0; l < levels; ++l) {
+            const int64_t vl = (int64_t)v * levels + l;
+            wpar_of(vl, v, win_ptr, win_idx, par_ptr, par_idx, buf);
+            if (idx_out)
+                for (size_t k = 0; k < buf.size(); ++k) idx_out[pos + (int64_t)k] = buf[k];
+            pos += (int64_t)buf.size();
+            if (ptr_out) ptr_out[vl + 1] = pos;
+        }
+    }
+    *n_out = pos;
+    return 0;
+}
+
 }  // extern "C"

@@ -184,6 +184,23 @@ __global__ void fate_prepare_stage_kernel(fate_bank b, fate_weights w, fate_deri
     }
     out.mean_base[g] = tot.result() / (double)n;
 
+    // stateless-row sums for the zero-cached-token class under uniform speed:
+    // full batch and the two k=2 shards (costs.py:257, :404-405)
+    if (out.row0_sums) {
+        PySum all, s0, s1;
+        const int half = nq / 2 + (nq % 2);
+        for (int q = 0; q < nq; ++q) {
+            const double x = qc_value(b.st_prompt[g], b.q_prompt[q0 + q], pcoef, pscale, decode,
+                                      cplx, b.dev_speed[0]);
+            all.add(x);
+            if (q < half) s0.add(x);
+            else s1.add(x);
+        }
+        out.row0_sums[(size_t)g * 3 + 0] = all.result();
+        out.row0_sums[(size_t)g * 3 + 1] = s0.result();
+        out.row0_sums[(size_t)g * 3 + 2] = s1.result();
+    }
+
     double split = 0.0;
     for (int e = b.ch_ptr[g]; e < b.ch_ptr[g + 1]; ++e) {
         const int c = b.ch_idx[e];
@@ -501,18 +518,40 @@ __global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weigh
 #include "fate_score_v3.cuh"
 #include "fate_score_v4.cuh"
 
+template <int DPL, int MINB>
+int launch_v4_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+                 const fate_derived* der, const fate_state* st, const fate_work* work,
+                 const fate_out* out, cudaStream_t s) {
+    const size_t smem = v4_item_bytes(bank->n_devices, bank->max_queries, win->max_level_ops) * 4;
+    if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v4 shared-memory footprint too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fate_score_v4_kernel<DPL, MINB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const unsigned blocks = (unsigned)((work->n_items + 3) / 4);
+    fate_score_v4_kernel<DPL, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st, *work,
+                                                               *out);
+    return 0;
+}
+
+// register budget (A/B only): FATE_MINB = 1 (default) | 6 | 8 CTAs per SM
+int v4_minb() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FATE_MINB");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
 template <int DPL>
 int launch_v4(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
               const fate_derived* der, const fate_state* st, const fate_work* work,
               const fate_out* out, cudaStream_t s) {
-    const size_t smem = v4_item_bytes(bank->n_devices, bank->max_queries, win->max_level_ops) * 4;
-    if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v4 shared-memory footprint too large");
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fate_score_v4_kernel<DPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    const unsigned blocks = (unsigned)((work->n_items + 3) / 4);
-    fate_score_v4_kernel<DPL><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st, *work, *out);
-    return 0;
+    switch (v4_minb()) {
+        case 6: return launch_v4_mb<DPL, 6>(bank, w, win, der, st, work, out, s);
+        case 8: return launch_v4_mb<DPL, 8>(bank, w, win, der, st, work, out, s);
+        default: return launch_v4_mb<DPL, 1>(bank, w, win, der, st, work, out, s);
+    }
 }
 
 template <int G>

@@ -100,8 +100,8 @@ __device__ __forceinline__ double v4_qc(const fate_bank& b, const V4Item& it, co
     return qc_value(sp, qp, it.pcoef, it.pscale, it.decode, it.cplx, b.dev_speed[dv]);
 }
 
-template <int DPL>
-__global__ void __launch_bounds__(128) fate_score_v4_kernel(fate_bank b, fate_weights w,
+template <int DPL, int MINB>
+__global__ void __launch_bounds__(128, MINB) fate_score_v4_kernel(fate_bank b, fate_weights w,
                                                             fate_windows win, fate_derived der,
                                                             fate_state st, fate_work work,
                                                             fate_out out) {
@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(128) fate_score_v4_kernel(fate_bank b, fate_we
     for (int j = 0; j < DPL; ++j)
         rep_m |= (unsigned long long)__ballot_sync(FULL, ok[j] && rep[j] == dv[j]) << (32 * j);
     const int n_cls = __popcll(rep_m);
-    const int n_rows = n_cls < V4_RCAP ? n_cls : V4_RCAP;
     int cls[DPL];
 #pragma unroll
     for (int j = 0; j < DPL; ++j) {
@@ -242,13 +241,6 @@ __global__ void __launch_bounds__(128) fate_score_v4_kernel(fate_bank b, fate_we
             V.rowc[dv[j]] = cls[j];
             if (rep[j] == dv[j]) V.rowdev[cls[j]] = dv[j];
         }
-    }
-    __syncwarp();
-
-    // ---- P2: class rows and sums ---------------------------------------------------------
-    for (int p = t; p < n_rows * nq; p += 32) {
-        const int c = p / nq, q = p - c * nq;
-        V.rows[c * Bmax + q] = v4_qc(b, it, V, V.rowdev[c], q);
     }
     const int n_idle = __popcll(idle_m);
     int kb = 0, ki = 0;
@@ -259,22 +251,60 @@ __global__ void __launch_bounds__(128) fate_score_v4_kernel(fate_bank b, fate_we
     const bool kb_ok = kb >= 2 && kb <= V4_KT;
     const bool ki_ok = ki != kb && ki >= 2 && ki <= V4_KT;
     const int per = 1 + (kb_ok ? kb : 0) + (ki_ok ? ki : 0);
+    // the zero-cached-token class under uniform speed is the stateless row:
+    // its sums come from the prologue table (row0_sums)
+    int cz = -1;
+    if ((b.flags & FATE_BANK_UNIFORM_SPEED) && !per_device_rows && kb <= 2 && ki <= 2) {
+        unsigned long long zm = 0ull;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j)
+            zm |= (unsigned long long)__ballot_sync(FULL, ok[j] && rep[j] == dv[j] && cs[j] == 0)
+                  << (32 * j);
+        if (zm) cz = __popcll(rep_m & low_mask(__ffsll((long long)zm) - 1));
+    }
+    const int n_cap = n_cls < V4_RCAP ? n_cls : V4_RCAP;       // classes with table slots
+    const int n_rows = n_cap - ((cz >= 0 && cz < V4_RCAP) ? 1 : 0);  // classes needing a row
+    __syncwarp();
+
+    // ---- P2: class rows and sums ---------------------------------------------------------
+    // row slot r <-> class r + (r >= cz) (the static class has no row)
+    for (int p = t; p < n_rows * nq; p += 32) {
+        const int r = p / nq, q = p - r * nq;
+        const int c = r + ((cz >= 0 && r >= cz) ? 1 : 0);
+        V.rows[r * Bmax + q] = v4_qc(b, it, V, V.rowdev[c], q);
+    }
+    if (t == 0 && cz >= 0) {
+        const double* z = der.row0_sums + (size_t)v * 3;
+        V.aware[cz] = z[0];
+        if (cz < V4_RCAP) {
+            if (kb == 2) {
+                V.shard[(cz * 2 + 0) * V4_KT + 0] = z[1];
+                V.shard[(cz * 2 + 0) * V4_KT + 1] = z[2];
+            }
+            if (ki == 2 && ki != kb) {
+                V.shard[(cz * 2 + 1) * V4_KT + 0] = z[1];
+                V.shard[(cz * 2 + 1) * V4_KT + 1] = z[2];
+            }
+        }
+    }
     __syncwarp();
     {
         const int n_row_tasks = n_rows * per;
-        const int n_tasks = n_row_tasks + (n_cls - n_rows);
+        const int n_tasks = n_row_tasks + (n_cls - n_cap);
         for (int p = t; p < n_tasks; p += 32) {
             PySum acc;
-            if (p >= n_row_tasks) {  // class without a shared row: direct aware
-                const int c = n_rows + (p - n_row_tasks);
+            if (p >= n_row_tasks) {  // class without a table slot: direct aware
+                const int c = n_cap + (p - n_row_tasks);
+                if (c == cz) continue;
                 const int dd = V.rowdev[c];
                 for (int q = 0; q < nq; ++q) acc.add(v4_qc(b, it, V, dd, q));
                 V.aware[c] = acc.result();
                 continue;
             }
-            const int c = p / per;
-            int j = p - c * per;
-            const double* row = V.rows + c * Bmax;
+            const int r = p / per;
+            const int c = r + ((cz >= 0 && r >= cz) ? 1 : 0);
+            int j = p - r * per;
+            const double* row = V.rows + r * Bmax;
             if (j == 0) {
                 for (int q = 0; q < nq; ++q) acc.add(row[q]);
                 V.aware[c] = acc.result();
@@ -309,23 +339,20 @@ __global__ void __launch_bounds__(128) fate_score_v4_kernel(fate_bank b, fate_we
             const long long hi = win.ptr[(long long)v * LV + l + 1];
             if (hi == lo) continue;
             const int n_b = (int)(hi - lo);
-            int located = 0;
-            if (!no_loc) {
-                for (int jx = t; jx < n_b; jx += 32) {
-                    const int x = win.idx[lo + jx];
-                    const int e1 = b.par_ptr[x + 1];
-                    for (int e = b.par_ptr[x]; e < e1; ++e) {
-                        const int pp = b.par_idx[e];
-                        located += pp != v && loc_row[pp] >= 0;
-                    }
-                }
-            }
+            const long long vl = (long long)v * LV + l;
             double aff[DPL];
-            if (!__any_sync(FULL, located > 0)) {
-                const double* row = der.tail_static + ((long long)v * LV + l) * M1;
+            {
+                const double* row = der.tail_static + vl * M1;
 #pragma unroll
                 for (int j = 0; j < DPL; ++j) aff[j] = row[1 + dmc[j]];
-            } else {
+            }
+            bool located = false;
+            if (!no_loc) {
+                const long long w1 = win.wpar_ptr[vl + 1];
+                for (long long i = win.wpar_ptr[vl] + t; i < w1; i += 32)
+                    located |= loc_row[win.wpar_idx[i]] >= 0;
+            }
+            if (__any_sync(FULL, located)) {
                 int base = 0;
                 for (int j0 = 0; j0 < n_b; j0 += 32) {
                     const int jx = j0 + t;
@@ -480,14 +507,16 @@ __global__ void __launch_bounds__(128) fate_score_v4_kernel(fate_bank b, fate_we
                     }
                     const int cd = V.rowc[dev];
                     double ssum;
-                    if (tab && cd < n_rows) {
+                    if (tab && cd < V4_RCAP) {
                         ssum = V.shard[(cd * 2 + kslot) * V4_KT + i];
                     } else {
+                        const int r = (cd < V4_RCAP && cd != cz) ? cd - ((cz >= 0 && cd > cz) ? 1 : 0)
+                                                                : -1;
                         int lo, hi;
                         shard_range(nq, k, i, &lo, &hi);
                         PySum acc;
                         for (int q = lo; q < hi; ++q)
-                            acc.add(cd < n_rows ? V.rows[cd * Bmax + q] : v4_qc(b, it, V, dev, q));
+                            acc.add(r >= 0 ? V.rows[r * Bmax + q] : v4_qc(b, it, V, dev, q));
                         ssum = acc.result();
                     }
                     const double tot = V.sw[dev] + V.tr[dev] + ssum;

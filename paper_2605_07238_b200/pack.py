@@ -40,6 +40,7 @@ ABL_BITS = {
     "no_prefix": 8,
     "no_shard": 16,
 }
+BANK_UNIFORM_SPEED = 1
 STAGE_CACHE_REUSE = 1
 STAGE_KEEP_CACHE = 2
 
@@ -252,6 +253,7 @@ def pack_bank(instances, models, topo) -> PackedBank:
         n_devices=n_dev, n_models=len(catalog), n_roles=len(role_rows), has_overrides=has_over,
         n_instances=len(instances), n_stages=g0, n_edges=int(arrays["par_idx"].size),
         n_queries=len(q_prompt), max_queries=max_q, beta_default=float(topo.default_transfer_coeff),
+        flags=BANK_UNIFORM_SPEED if bool(np.all(speed == speed[0])) else 0,
     )
     return PackedBank(
         device_ids=device_ids, dev_index=dev_index, model_index=model_index,

@@ -51,6 +51,9 @@ def load_library():
     L.fate_windows_build_host.restype = C.c_int
     L.fate_windows_build_host.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_int32, C.c_void_p, C.c_void_p]
+    L.fate_window_parents_host.restype = C.c_int
+    L.fate_window_parents_host.argtypes = [C.c_int32, C.c_int32] + [C.c_void_p] * 6 + [
+        C.POINTER(C.c_int64)]
     L.fate_prepare.restype = C.c_int
     L.fate_prepare.argtypes = [C.c_void_p] * 5
     L.fate_score.restype = C.c_int
@@ -93,6 +96,30 @@ def build_windows(packed: PackedBank, levels: int):
                                      idx.ctypes.data), "windows_build")
     packed.windows[levels] = (ptr, idx)
     return ptr, idx
+
+
+def build_window_parents(packed: PackedBank, levels: int):
+    """Distinct window parents per (stage, level) via the native builder."""
+    key = ("wpar", levels)
+    if key in packed.windows:
+        return packed.windows[key]
+    L = load_library()
+    ptr, idx = build_windows(packed, levels)
+    a = packed.arrays
+    n = packed.n_stages
+    par_ptr = np.ascontiguousarray(a["par_ptr"])
+    par_idx = np.ascontiguousarray(a["par_idx"])
+    cnt = C.c_int64(0)
+    _check(L.fate_window_parents_host(n, levels, ptr.ctypes.data, idx.ctypes.data,
+                                      par_ptr.ctypes.data, par_idx.ctypes.data, None, None,
+                                      C.byref(cnt)), "window_parents_count")
+    wptr = np.zeros(n * levels + 1, dtype=np.int64)
+    widx = np.zeros(max(cnt.value, 1), dtype=np.int32)
+    _check(L.fate_window_parents_host(n, levels, ptr.ctypes.data, idx.ctypes.data,
+                                      par_ptr.ctypes.data, par_idx.ctypes.data, wptr.ctypes.data,
+                                      widx.ctypes.data, C.byref(cnt)), "window_parents_build")
+    packed.windows[key] = (wptr, widx)
+    return wptr, widx
 
 
 def max_level_ops(packed: PackedBank, levels: int) -> int:
@@ -166,9 +193,14 @@ class DeviceBank:
         ptr, idx = build_windows(packed, self.levels)
         self.win_ptr = _to_dev(torch, ptr, self.device)
         self.win_idx = _to_dev(torch, idx, self.device)
+        wptr, widx = build_window_parents(packed, self.levels)
+        self.wpar_ptr = _to_dev(torch, wptr, self.device)
+        self.wpar_idx = _to_dev(torch, widx, self.device)
         self.cwin = abi.FateWindows(levels=self.levels,
                                     max_level_ops=max_level_ops(packed, self.levels),
-                                    ptr=self.win_ptr.data_ptr(), idx=self.win_idx.data_ptr())
+                                    ptr=self.win_ptr.data_ptr(), idx=self.win_idx.data_ptr(),
+                                    wpar_ptr=self.wpar_ptr.data_ptr(),
+                                    wpar_idx=self.wpar_idx.data_ptr())
         n, e = packed.n_stages, packed.scalars["n_edges"]
         f64 = dict(dtype=torch.float64, device=self.device)
         self.mean_base = torch.empty(max(n, 1), **f64)
@@ -176,6 +208,7 @@ class DeviceBank:
         self.split_penalty = torch.empty(max(n, 1), **f64)
         self.edge_sigma = torch.empty(max(e, 1), **f64)
         self.edge_term = torch.empty(max(e, 1), **f64)
+        self.row0_sums = torch.empty(max(n * 3, 1), **f64)
         n_static = n * self.levels * (packed.scalars["n_models"] + 1)
         self.tail_static = torch.empty(max(n_static, 1), **f64)
         self.cder = abi.FateDerived(mean_base=self.mean_base.data_ptr(),
@@ -183,6 +216,7 @@ class DeviceBank:
                                     split_penalty=self.split_penalty.data_ptr(),
                                     edge_sigma=self.edge_sigma.data_ptr(),
                                     edge_term=self.edge_term.data_ptr(),
+                                    row0_sums=self.row0_sums.data_ptr(),
                                     tail_static=self.tail_static.data_ptr())
         s = stream or torch.cuda.current_stream(self.device)
         _check(L.fate_prepare(C.byref(self.cbank), C.byref(self.cweights), C.byref(self.cwin),
