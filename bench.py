@@ -433,6 +433,7 @@ def run_fate(args):
     dstates = dbank.upload_states(states)
     dwork = dbank.upload_work(work)
     out = dbank.alloc_out(work, extras=True)
+    out.tail = None  # diagnostic only; Psi + S + completion are what FATE consumes
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MiB
     torch.cuda.synchronize(device)
 
@@ -504,6 +505,7 @@ def measure_c4(torch, device, args) -> dict:
     dstates = dbank.upload_states(states)
     dwork = dbank.upload_work(work)
     out = dbank.alloc_out(work, extras=True)
+    out.tail = None
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)
     clocks = ClockSampler(device.index or 0)
     ms, launches = time_device(torch, dbank, dstates, dwork, out, max(5, args.steps // 4),

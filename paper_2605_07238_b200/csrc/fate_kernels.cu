@@ -533,21 +533,23 @@ int launch_v4_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     return 0;
 }
 
-// register budget (A/B only): FATE_MINB = 1 (default) | 6 | 8 CTAs per SM
-int v4_minb() {
+// register budget: CTAs per SM the register allocation must allow.  Measured
+// on B200 (profiles/): 8 for one device slot per lane (<= 64 registers), 6 for
+// two (<= 80).  FATE_MINB = 1 | 6 | 8 overrides for A/B runs.
+int v4_minb(int dpl) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FATE_MINB");
-        v = e ? atoi(e) : 1;
+        v = e ? atoi(e) : 0;
     }
-    return v;
+    return v ? v : (dpl == 1 ? 8 : 6);
 }
 
 template <int DPL>
 int launch_v4(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
               const fate_derived* der, const fate_state* st, const fate_work* work,
               const fate_out* out, cudaStream_t s) {
-    switch (v4_minb()) {
+    switch (v4_minb(DPL)) {
         case 6: return launch_v4_mb<DPL, 6>(bank, w, win, der, st, work, out, s);
         case 8: return launch_v4_mb<DPL, 8>(bank, w, win, der, st, work, out, s);
         default: return launch_v4_mb<DPL, 1>(bank, w, win, der, st, work, out, s);
