@@ -173,9 +173,11 @@ typedef struct fate_derived {
     double* split_penalty;          /* [n_stages] slot>=1 split penalty */
     double* edge_sigma;             /* [n_edges] sigma(par_idx[e] -> child) */
     double* edge_term;              /* [n_edges] tail locality term at beta_default */
-    double* row0_sums;              /* [n_stages*3] stateless-row Neumaier sums: full batch,
-                                       k=2 shards 0 and 1 (valid when bank flags has
-                                       FATE_BANK_UNIFORM_SPEED) */
+    double* row_sums;               /* [n_stages*6] Neumaier sums (full batch, k=2 shard 0,
+                                       shard 1) of the stateless row (stage part P) and of
+                                       the full-hit row (stage part 0); valid under
+                                       FATE_BANK_UNIFORM_SPEED (costs.py:257, :404-405) */
+    int32_t* inst_qgroups;          /* [n_instances] 1 if any query has a prefix group */
     double* tail_static;            /* [n_stages*levels*(n_models+1)] affinity chain per
                                        (stage, level, displacement class) with no locality
                                        op applied (costs.py:307-331) */

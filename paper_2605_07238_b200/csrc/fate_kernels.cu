@@ -184,21 +184,31 @@ __global__ void fate_prepare_stage_kernel(fate_bank b, fate_weights w, fate_deri
     }
     out.mean_base[g] = tot.result() / (double)n;
 
-    // stateless-row sums for the zero-cached-token class under uniform speed:
-    // full batch and the two k=2 shards (costs.py:257, :404-405)
-    if (out.row0_sums) {
-        PySum all, s0, s1;
+    // Neumaier sums of the stateless row (stage part P) and of the full-hit row
+    // (stage part 0) under uniform speed: full batch and the two k=2 shards
+    // (costs.py:257, :404-405)
+    if (out.row_sums) {
         const int half = nq / 2 + (nq % 2);
-        for (int q = 0; q < nq; ++q) {
-            const double x = qc_value(b.st_prompt[g], b.q_prompt[q0 + q], pcoef, pscale, decode,
-                                      cplx, b.dev_speed[0]);
-            all.add(x);
-            if (q < half) s0.add(x);
-            else s1.add(x);
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {
+            const long long sp = which == 0 ? b.st_prompt[g] : 0;
+            PySum all, s0, s1;
+            for (int q = 0; q < nq; ++q) {
+                const double x = qc_value(sp, b.q_prompt[q0 + q], pcoef, pscale, decode, cplx,
+                                          b.dev_speed[0]);
+                all.add(x);
+                if (q < half) s0.add(x);
+                else s1.add(x);
+            }
+            out.row_sums[(size_t)g * 6 + 3 * which + 0] = all.result();
+            out.row_sums[(size_t)g * 6 + 3 * which + 1] = s0.result();
+            out.row_sums[(size_t)g * 6 + 3 * which + 2] = s1.result();
         }
-        out.row0_sums[(size_t)g * 3 + 0] = all.result();
-        out.row0_sums[(size_t)g * 3 + 1] = s0.result();
-        out.row0_sums[(size_t)g * 3 + 2] = s1.result();
+    }
+    if (out.inst_qgroups && g == b.inst_stage_off[inst]) {
+        int any = 0;
+        for (int q = 0; q < nq; ++q) any |= b.q_group[q0 + q] != -1;
+        out.inst_qgroups[inst] = any;
     }
 
     double split = 0.0;

@@ -40,7 +40,7 @@ struct V4Op {
 
 struct V4View {
     double* rows;     // [RCAP*Bmax]
-    double* shard;    // [RCAP*2*KT]
+    double* shard;    // [D*2*KT] per class
     double* aware;    // [D] per class
     double* sw;       // [D]
     double* tr;       // [D]
@@ -48,12 +48,13 @@ struct V4View {
     int* key;         // [D] cs per device
     int* rowc;        // [D] class per device
     int* rowdev;      // [D] representative per class
+    int* slot2cls;    // [RCAP] class of each shared-memory row slot
 };
 
 __host__ __device__ inline size_t v4_item_bytes(int D, int Bmax, int ops_cap) {
-    size_t dbl = (size_t)V4_RCAP * Bmax + (size_t)V4_RCAP * 2 * V4_KT + 3 * (size_t)D;
+    size_t dbl = (size_t)V4_RCAP * Bmax + (size_t)D * 2 * V4_KT + 3 * (size_t)D;
     size_t ops = (size_t)ops_cap * sizeof(V4Op);
-    size_t ints = 3 * (size_t)D;
+    size_t ints = 3 * (size_t)D + V4_RCAP;
     return (dbl * 8 + ops + ints * 4 + 15) & ~size_t(15);
 }
 
@@ -61,7 +62,7 @@ __device__ inline V4View v4_view(unsigned char* base, int D, int Bmax, int ops_c
     V4View v;
     double* dp = reinterpret_cast<double*>(base);
     v.rows = dp; dp += (size_t)V4_RCAP * Bmax;
-    v.shard = dp; dp += (size_t)V4_RCAP * 2 * V4_KT;
+    v.shard = dp; dp += (size_t)D * 2 * V4_KT;
     v.aware = dp; dp += D;
     v.sw = dp; dp += D;
     v.tr = dp; dp += D;
@@ -69,7 +70,8 @@ __device__ inline V4View v4_view(unsigned char* base, int D, int Bmax, int ops_c
     int* ip = reinterpret_cast<int*>(v.ops + ops_cap);
     v.key = ip; ip += D;
     v.rowc = ip; ip += D;
-    v.rowdev = ip;
+    v.rowdev = ip; ip += D;
+    v.slot2cls = ip;
     return v;
 }
 
@@ -86,11 +88,8 @@ struct V4Item {
 // cache-aware query_compute of query q on device dv (costs.py:70-94)
 __device__ __forceinline__ double v4_qc(const fate_bank& b, const V4Item& it, const V4View& V,
                                         int dv, int q) {
-    long long sp = it.Pv, qp = b.q_prompt[it.q0 + q];
-    if (it.cache_reuse) {
-        const long long cc = V.key[dv];
-        sp = sp - cc > 0 ? sp - cc : 0;
-    }
+    const long long sp = V.key[dv];  // max(0, P(v) - cached stage-group tokens)
+    long long qp = b.q_prompt[it.q0 + q];
     const int qg = b.q_group[it.q0 + q];
     if (qg != -1) {
         const long long drow = it.dev_row0 + dv;
@@ -168,8 +167,11 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v4_kernel(fate_bank b, f
             const long long row = it.dev_row0 + dv[j];
             res[j] = st.residency[row];
             fr[j] = st.dev_free[row];
-            if (it.cache_reuse)
-                cs[j] = cached_tokens(st.kappa + row * it.cap4, st.kappa_n[row], it.gv, m);
+            cs[j] = it.Pv;  // effective stage part sp = max(0, P - cached), costs.py:86-88
+            if (it.cache_reuse) {
+                const int c = cached_tokens(st.kappa + row * it.cap4, st.kappa_n[row], it.gv, m);
+                cs[j] = it.Pv - c > 0 ? it.Pv - c : 0;
+            }
             V.key[dv[j]] = cs[j];
             V.sw[dv[j]] = (m < 0 || res[j] == m) ? 0.0 : b.model_switch[m] * w.switch_x;
         }
@@ -187,9 +189,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v4_kernel(fate_bank b, f
 #pragma unroll
     for (int j = 0; j < DPL; ++j)
         if (live[j]) V.tr[dv[j]] = trv[j] * w.transfer_x;
-    bool qg_any = false;
-    for (int q = t; q < nq; q += 32) qg_any |= b.q_group[it.q0 + q] != -1;
-    const bool per_device_rows = __any_sync(FULL, qg_any);
+    const bool per_device_rows = der.inst_qgroups[inst] != 0;
     unsigned long long idle_m = 0ull, ok_m = 0ull;
 #pragma unroll
     for (int j = 0; j < DPL; ++j) {
@@ -251,58 +251,74 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v4_kernel(fate_bank b, f
     const bool kb_ok = kb >= 2 && kb <= V4_KT;
     const bool ki_ok = ki != kb && ki >= 2 && ki <= V4_KT;
     const int per = 1 + (kb_ok ? kb : 0) + (ki_ok ? ki : 0);
-    // the zero-cached-token class under uniform speed is the stateless row:
-    // its sums come from the prologue table (row0_sums)
-    int cz = -1;
+    // static classes (uniform speed, no query prefix groups): the stateless row
+    // sp = P (class A) and the full-hit row sp = 0 (class B) have their sums in
+    // the prologue table row_sums[v][0..5]
+    int cA = -1, cB = -1;
     if ((b.flags & FATE_BANK_UNIFORM_SPEED) && !per_device_rows && kb <= 2 && ki <= 2) {
-        unsigned long long zm = 0ull;
+        unsigned long long am = 0ull, bm = 0ull;
 #pragma unroll
-        for (int j = 0; j < DPL; ++j)
-            zm |= (unsigned long long)__ballot_sync(FULL, ok[j] && rep[j] == dv[j] && cs[j] == 0)
-                  << (32 * j);
-        if (zm) cz = __popcll(rep_m & low_mask(__ffsll((long long)zm) - 1));
+        for (int j = 0; j < DPL; ++j) {
+            const bool r0 = ok[j] && rep[j] == dv[j];
+            am |= (unsigned long long)__ballot_sync(FULL, r0 && cs[j] == it.Pv) << (32 * j);
+            bm |= (unsigned long long)__ballot_sync(FULL, r0 && cs[j] == 0 && it.Pv > 0) << (32 * j);
+        }
+        if (am) cA = __popcll(rep_m & low_mask(__ffsll((long long)am) - 1));
+        if (bm) cB = __popcll(rep_m & low_mask(__ffsll((long long)bm) - 1));
     }
-    const int n_cap = n_cls < V4_RCAP ? n_cls : V4_RCAP;       // classes with table slots
-    const int n_rows = n_cap - ((cz >= 0 && cz < V4_RCAP) ? 1 : 0);  // classes needing a row
-    __syncwarp();
-
-    // ---- P2: class rows and sums ---------------------------------------------------------
-    // row slot r <-> class r + (r >= cz) (the static class has no row)
-    for (int p = t; p < n_rows * nq; p += 32) {
-        const int r = p / nq, q = p - r * nq;
-        const int c = r + ((cz >= 0 && r >= cz) ? 1 : 0);
-        V.rows[r * Bmax + q] = v4_qc(b, it, V, V.rowdev[c], q);
-    }
-    if (t == 0 && cz >= 0) {
-        const double* z = der.row0_sums + (size_t)v * 3;
-        V.aware[cz] = z[0];
-        if (cz < V4_RCAP) {
+    // dynamic classes: rows in shared memory for the first RCAP of them
+    unsigned long long dyn_m = n_cls >= 64 ? ~0ull : ((1ull << n_cls) - 1ull);
+    if (cA >= 0) dyn_m &= ~(1ull << cA);
+    if (cB >= 0) dyn_m &= ~(1ull << cB);
+    const int n_dyn = __popcll(dyn_m);
+    const int n_rows = n_dyn < V4_RCAP ? n_dyn : V4_RCAP;
+    if (t == 0) {
+        unsigned long long mm = dyn_m;
+        for (int r = 0; r < n_rows; ++r) {
+            V.slot2cls[r] = __ffsll((long long)mm) - 1;
+            mm &= mm - 1;
+        }
+        const double* z = der.row_sums + (size_t)v * 6;
+#pragma unroll
+        for (int sidx = 0; sidx < 2; ++sidx) {
+            const int c = sidx == 0 ? cA : cB;
+            if (c < 0) continue;
+            const double* zz = z + 3 * sidx;
+            V.aware[c] = zz[0];
             if (kb == 2) {
-                V.shard[(cz * 2 + 0) * V4_KT + 0] = z[1];
-                V.shard[(cz * 2 + 0) * V4_KT + 1] = z[2];
+                V.shard[(c * 2 + 0) * V4_KT + 0] = zz[1];
+                V.shard[(c * 2 + 0) * V4_KT + 1] = zz[2];
             }
             if (ki == 2 && ki != kb) {
-                V.shard[(cz * 2 + 1) * V4_KT + 0] = z[1];
-                V.shard[(cz * 2 + 1) * V4_KT + 1] = z[2];
+                V.shard[(c * 2 + 1) * V4_KT + 0] = zz[1];
+                V.shard[(c * 2 + 1) * V4_KT + 1] = zz[2];
             }
         }
     }
     __syncwarp();
+
+    // ---- P2: dynamic class rows and sums -----------------------------------------------
+    for (int p = t; p < n_rows * nq; p += 32) {
+        const int r = p / nq, q = p - r * nq;
+        V.rows[r * Bmax + q] = v4_qc(b, it, V, V.rowdev[V.slot2cls[r]], q);
+    }
+    __syncwarp();
     {
         const int n_row_tasks = n_rows * per;
-        const int n_tasks = n_row_tasks + (n_cls - n_cap);
+        const int n_tasks = n_row_tasks + (n_dyn - n_rows);
         for (int p = t; p < n_tasks; p += 32) {
             PySum acc;
-            if (p >= n_row_tasks) {  // class without a table slot: direct aware
-                const int c = n_cap + (p - n_row_tasks);
-                if (c == cz) continue;
+            if (p >= n_row_tasks) {  // dynamic class beyond RCAP: direct aware
+                unsigned long long mm = dyn_m;
+                for (int r = 0; r < n_rows + (p - n_row_tasks); ++r) mm &= mm - 1;
+                const int c = __ffsll((long long)mm) - 1;
                 const int dd = V.rowdev[c];
                 for (int q = 0; q < nq; ++q) acc.add(v4_qc(b, it, V, dd, q));
                 V.aware[c] = acc.result();
                 continue;
             }
             const int r = p / per;
-            const int c = r + ((cz >= 0 && r >= cz) ? 1 : 0);
+            const int c = V.slot2cls[r];
             int j = p - r * per;
             const double* row = V.rows + r * Bmax;
             if (j == 0) {
@@ -422,17 +438,32 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v4_kernel(fate_bank b, f
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < DPL; ++j) aff[j] = 0.0;
-                for (int o = 0; o < base; ++o) {
-                    const V4Op op = V.ops[o];
+                if (!b.has_overrides) {
+                    // aff starts at +0.0 and, in round-to-nearest, never becomes -0.0, so
+                    // adding +0.0 for a skipped op leaves it bit-identical: branch-free walk
+#pragma unroll 4
+                    for (int o = 0; o < base; ++o) {
+                        const V4Op op = V.ops[o];
 #pragma unroll
-                    for (int j = 0; j < DPL; ++j) {
-                        if (op.kind == 0) {
-                            if (op.key != dv[j]) aff[j] += op.val;
-                        } else if (op.kind == 1) {
-                            if (op.key == dmc[j]) aff[j] += op.val;
-                        } else if (op.key != dv[j]) {
-                            aff[j] -= w.lambda_tr * b.beta[(size_t)op.key * D + (live[j] ? dv[j] : 0)] *
-                                      op.val * w.transfer_x * w.locality_scale;
+                        for (int j = 0; j < DPL; ++j) {
+                            const bool apply = op.kind == 1 ? op.key == dmc[j] : op.key != dv[j];
+                            aff[j] += apply ? op.val : 0.0;
+                        }
+                    }
+                } else {
+                    for (int o = 0; o < base; ++o) {
+                        const V4Op op = V.ops[o];
+#pragma unroll
+                        for (int j = 0; j < DPL; ++j) {
+                            if (op.kind == 0) {
+                                if (op.key != dv[j]) aff[j] += op.val;
+                            } else if (op.kind == 1) {
+                                if (op.key == dmc[j]) aff[j] += op.val;
+                            } else if (op.key != dv[j]) {
+                                aff[j] -= w.lambda_tr *
+                                          b.beta[(size_t)op.key * D + (live[j] ? dv[j] : 0)] *
+                                          op.val * w.transfer_x * w.locality_scale;
+                            }
                         }
                     }
                 }
@@ -472,7 +503,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v4_kernel(fate_bank b, f
 
         // prefix_overlap_thousands (costs.py:127-145), integer-exact
         long long tokens = 0;
-        if (it.cache_reuse) tokens += cs[j] < it.Pv ? cs[j] : it.Pv;
+        if (it.cache_reuse) tokens += it.Pv - cs[j];  // min(cached, P) = P - sp
         if (per_device_rows) {
             const long long row = it.dev_row0 + d;
             const int32_t* kap = st.kappa + row * it.cap4;
@@ -506,17 +537,18 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v4_kernel(fate_bank b, f
                         rest &= rest - 1;
                     }
                     const int cd = V.rowc[dev];
+                    const bool is_static = cd == cA || cd == cB;
+                    const int r = is_static ? -1 : __popcll(dyn_m & low_mask(cd));
+                    const int slot = (r >= 0 && r < n_rows) ? r : -1;
                     double ssum;
-                    if (tab && cd < V4_RCAP) {
+                    if (tab && (is_static || slot >= 0)) {
                         ssum = V.shard[(cd * 2 + kslot) * V4_KT + i];
                     } else {
-                        const int r = (cd < V4_RCAP && cd != cz) ? cd - ((cz >= 0 && cd > cz) ? 1 : 0)
-                                                                : -1;
                         int lo, hi;
                         shard_range(nq, k, i, &lo, &hi);
                         PySum acc;
                         for (int q = lo; q < hi; ++q)
-                            acc.add(r >= 0 ? V.rows[r * Bmax + q] : v4_qc(b, it, V, dev, q));
+                            acc.add(slot >= 0 ? V.rows[slot * Bmax + q] : v4_qc(b, it, V, dev, q));
                         ssum = acc.result();
                     }
                     const double tot = V.sw[dev] + V.tr[dev] + ssum;

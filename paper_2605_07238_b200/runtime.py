@@ -208,7 +208,9 @@ class DeviceBank:
         self.split_penalty = torch.empty(max(n, 1), **f64)
         self.edge_sigma = torch.empty(max(e, 1), **f64)
         self.edge_term = torch.empty(max(e, 1), **f64)
-        self.row0_sums = torch.empty(max(n * 3, 1), **f64)
+        self.row_sums = torch.empty(max(n * 6, 1), **f64)
+        self.inst_qgroups = torch.empty(max(packed.scalars["n_instances"], 1), dtype=torch.int32,
+                                        device=self.device)
         n_static = n * self.levels * (packed.scalars["n_models"] + 1)
         self.tail_static = torch.empty(max(n_static, 1), **f64)
         self.cder = abi.FateDerived(mean_base=self.mean_base.data_ptr(),
@@ -216,7 +218,8 @@ class DeviceBank:
                                     split_penalty=self.split_penalty.data_ptr(),
                                     edge_sigma=self.edge_sigma.data_ptr(),
                                     edge_term=self.edge_term.data_ptr(),
-                                    row0_sums=self.row0_sums.data_ptr(),
+                                    row_sums=self.row_sums.data_ptr(),
+                                    inst_qgroups=self.inst_qgroups.data_ptr(),
                                     tail_static=self.tail_static.data_ptr())
         s = stream or torch.cuda.current_stream(self.device)
         _check(L.fate_prepare(C.byref(self.cbank), C.byref(self.cweights), C.byref(self.cwin),
@@ -284,48 +287,98 @@ class DeviceWork:
 
 
 class HostPipeline:
-    """Reference-facing call with HOST buffers: per call, the scenario states
-    and work list are copied host->device from pinned memory, scored, and Psi
-    copied device->host into pinned memory -- all stream-ordered on one stream
-    (the static bank is HBM-resident, uploaded once like model weights)."""
+    """Reference-facing call with HOST buffers: each call copies the step's
+    scenario states and work list host->device from pinned memory, scores,
+    and copies Psi device->host into pinned memory.  The static bank stays
+    HBM-resident (uploaded once, like model weights).
+
+    The batch is split into ``n_chunks`` scenario-aligned chunks issued
+    round-robin on ``n_streams`` CUDA streams, so the H2D copy of chunk i+1,
+    the scoring of chunk i and the D2H copy of chunk i-1 overlap (copy engines
+    and SMs run concurrently).  Items must be scenario-major (as every work
+    list built by this package is)."""
 
     def __init__(self, dbank: DeviceBank, states: PackedStates, work: WorkList,
-                 extras: bool = False):
+                 extras: bool = False, n_chunks: int = 8, n_streams: int = 3):
         torch = dbank.torch
         self.dbank = dbank
-        self.host_in = {}
-        for k, v in states.arrays.items():
-            self.host_in["s:" + k] = torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+        D = dbank.packed.scalars["n_devices"]
+        cap4 = states.kappa_cap * 4
+        sc = np.asarray(work.scen)
+        if sc.size and np.any(np.diff(sc) < 0):
+            raise ValueError("HostPipeline needs a scenario-major work list")
+        if work.n_items and np.any(np.diff(work.psi_off) < 0):
+            raise ValueError("HostPipeline needs increasing psi offsets")
+        sa = states.arrays
+        self.host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+                     for k, v in sa.items()}
         for k in ("scen", "stage", "psi_off"):
-            self.host_in["w:" + k] = torch.from_numpy(
+            self.host["w:" + k] = torch.from_numpy(
                 np.ascontiguousarray(getattr(work, k))).pin_memory()
-        self.dev_in = {k: torch.empty_like(v, device=dbank.device) for k, v in self.host_in.items()}
+        self.dev = {k: torch.empty_like(v, device=dbank.device) for k, v in self.host.items()}
         self.cstate = abi.fill_struct(
             abi.FateState(), {"n_scenarios": states.n_scenarios, "kappa_cap": states.kappa_cap},
-            {k: self.dev_in["s:" + k].data_ptr() for k in abi.STATE_PTRS})
-        self.cwork = abi.fill_struct(abi.FateWork(), {"n_items": work.n_items},
-                                     {k: self.dev_in["w:" + k].data_ptr()
-                                      for k in ("scen", "stage", "psi_off")})
+            {k: self.dev[k].data_ptr() for k in abi.STATE_PTRS})
         self.out = dbank.alloc_out(work, extras=extras)
         self.host_psi = torch.empty(self.out.psi.shape, dtype=torch.float64).pin_memory()
-        self.h2d_bytes = sum(v.numel() * v.element_size() for v in self.host_in.values())
-        self.d2h_bytes = self.host_psi.numel() * 8
+        # scenario-aligned chunks
+        n = work.n_items
+        bounds = [0]
+        if n:
+            for c in range(1, n_chunks):
+                i = (n * c) // n_chunks
+                while 0 < i < n and sc[i] == sc[i - 1]:
+                    i += 1
+                if bounds[-1] < i < n:
+                    bounds.append(i)
+            bounds.append(n)
+        loc_off = np.asarray(sa["scen_loc_off"])
+        n_loc = sa["loc"].size
+        self.chunks = []
+        for i0, i1 in zip(bounds[:-1], bounds[1:]):
+            s0, s1 = int(sc[i0]), int(sc[i1 - 1]) + 1
+            l0 = int(loc_off[s0])
+            l1 = int(loc_off[s1]) if s1 < states.n_scenarios else n_loc
+            p0 = int(work.psi_off[i0])
+            p1 = int(work.psi_off[i1]) if i1 < n else work.n_psi
+            sl = {"scen_inst": (s0, s1), "scen_clock": (s0, s1), "scen_loc_off": (s0, s1),
+                  "loc": (l0, l1), "residency": (s0 * D, s1 * D), "dev_free": (s0 * D, s1 * D),
+                  "kappa_n": (s0 * D, s1 * D), "kappa": (s0 * D * cap4, s1 * D * cap4),
+                  "w:scen": (i0, i1), "w:stage": (i0, i1), "w:psi_off": (i0, i1)}
+            cw = abi.fill_struct(abi.FateWork(), {"n_items": i1 - i0}, {
+                k: self.dev["w:" + k].data_ptr() + i0 * self.dev["w:" + k].element_size()
+                for k in ("scen", "stage", "psi_off")})
+            self.chunks.append((sl, cw, (p0, p1)))
+        self.streams = [torch.cuda.Stream(dbank.device) for _ in range(max(1, n_streams))]
+        self.h2d_bytes = sum(v.numel() * v.element_size() for v in self.host.values())
+        self.d2h_bytes = work.n_psi * 8
 
     def run(self, stream=None):
         torch = self.dbank.torch
-        s = stream or torch.cuda.current_stream(self.dbank.device)
-        with torch.cuda.stream(s):
-            for k, v in self.host_in.items():
-                self.dev_in[k].copy_(v, non_blocking=True)
-            cout = abi.FateOut(psi=self.out.psi.data_ptr(),
-                               sched=self.out.sched.data_ptr() if self.out.sched is not None else None,
-                               tail=self.out.tail.data_ptr() if self.out.tail is not None else None,
-                               completion=(self.out.completion.data_ptr()
-                                           if self.out.completion is not None else None))
-            d = self.dbank
-            _check(load_library().fate_score(
-                C.byref(d.cbank), C.byref(d.cweights), C.byref(d.cwin), C.byref(d.cder),
-                C.byref(self.cstate), C.byref(self.cwork), C.byref(cout),
-                C.c_void_p(s.cuda_stream)), "fate_score")
-            self.host_psi.copy_(self.out.psi, non_blocking=True)
+        main = stream or torch.cuda.current_stream(self.dbank.device)
+        start = torch.cuda.Event()
+        start.record(main)
+        d = self.dbank
+        L = load_library()
+        cout = abi.FateOut(psi=self.out.psi.data_ptr(),
+                           sched=self.out.sched.data_ptr() if self.out.sched is not None else None,
+                           tail=self.out.tail.data_ptr() if self.out.tail is not None else None,
+                           completion=(self.out.completion.data_ptr()
+                                       if self.out.completion is not None else None))
+        for c, (sl, cw, (p0, p1)) in enumerate(self.chunks):
+            s = self.streams[c % len(self.streams)]
+            s.wait_event(start)
+            with torch.cuda.stream(s):
+                for k, (a, b_) in sl.items():
+                    if b_ > a:
+                        self.dev[k][a:b_].copy_(self.host[k][a:b_], non_blocking=True)
+                _check(L.fate_score(C.byref(d.cbank), C.byref(d.cweights), C.byref(d.cwin),
+                                    C.byref(d.cder), C.byref(self.cstate), C.byref(cw),
+                                    C.byref(cout), C.c_void_p(s.cuda_stream)), "fate_score")
+                if p1 > p0:
+                    self.host_psi[p0:p1].copy_(self.out.psi[p0:p1], non_blocking=True)
+        for s in self.streams:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            main.wait_event(ev)
         return self.host_psi

@@ -81,3 +81,18 @@ def test_library_is_native():
     _gpu(edge_case(horizon=2))
     assert runtime.launch_count() > before
     assert runtime.LIB_PATH.endswith("paper_2605_07238_b200/libfate.so")
+
+
+def test_host_pipeline_chunks_match_device_path():
+    """The pinned host-buffer call (chunked over 3 streams) returns exactly the
+    device-resident result."""
+    case = c5_case(n_inst=5)
+    dbank = runtime.DeviceBank(case.bank, case.weights)
+    want = dbank.score(case.states, case.work, extras=False).psi.cpu().numpy()[: case.work.n_psi]
+    pipe = runtime.HostPipeline(dbank, case.states, case.work, n_chunks=4, n_streams=3)
+    got = pipe.run()
+    import torch
+
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(got.numpy()[: case.work.n_psi]), bits(want))
+    assert len(pipe.chunks) >= 2
