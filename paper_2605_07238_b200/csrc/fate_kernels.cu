@@ -527,6 +527,22 @@ __global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weigh
 
 #include "fate_score_v3.cuh"
 #include "fate_score_v4.cuh"
+#include "fate_score_v5.cuh"
+
+template <int DPL, int MINB>
+int launch_v5_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+                 const fate_derived* der, const fate_state* st, const fate_work* work,
+                 const fate_out* out, cudaStream_t s) {
+    const size_t smem = v5_item_bytes(bank->n_devices, bank->max_queries, win->max_level_ops) * 4;
+    if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v5 shared-memory footprint too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fate_score_v5_kernel<DPL, MINB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const unsigned blocks = (unsigned)((work->n_items + 3) / 4);
+    fate_score_v5_kernel<DPL, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st, *work,
+                                                               *out);
+    return 0;
+}
 
 template <int DPL, int MINB>
 int launch_v4_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
@@ -556,6 +572,17 @@ int v4_minb(int dpl) {
 }
 
 template <int DPL>
+int launch_v5(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+              const fate_derived* der, const fate_state* st, const fate_work* work,
+              const fate_out* out, cudaStream_t s) {
+    switch (v4_minb(DPL)) {
+        case 1: return launch_v5_mb<DPL, 1>(bank, w, win, der, st, work, out, s);
+        case 6: return launch_v5_mb<DPL, 6>(bank, w, win, der, st, work, out, s);
+        default: return launch_v5_mb<DPL, 8>(bank, w, win, der, st, work, out, s);
+    }
+}
+
+template <int DPL>
 int launch_v4(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
               const fate_derived* der, const fate_state* st, const fate_work* work,
               const fate_out* out, cudaStream_t s) {
@@ -581,12 +608,15 @@ int launch_v3(const fate_bank* bank, const fate_weights* w, const fate_windows* 
     return 0;
 }
 
-// Kernel generation (A/B benchmarking only): FATE_SCORE_KERNEL=v1|v3, default v4.
+// Kernel generation (A/B benchmarking only): FATE_SCORE_KERNEL=v1|v3|v4, default v5.
 int kernel_gen() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FATE_SCORE_KERNEL");
-        v = (e && strcmp(e, "v1") == 0) ? 1 : (e && strcmp(e, "v3") == 0) ? 3 : 4;
+        v = (e && strcmp(e, "v1") == 0)   ? 1
+            : (e && strcmp(e, "v3") == 0) ? 3
+            : (e && strcmp(e, "v4") == 0) ? 4
+                                          : 5;
     }
     return v;
 }
@@ -671,7 +701,11 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int D = bank->n_devices;
     const size_t per_item = item_smem_bytes(D, bank->max_queries);
-    if (kernel_gen() == 4) {
+    if (kernel_gen() == 5) {
+        rc = D <= 32 ? launch_v5<1>(bank, w, win, der, st, work, out, s)
+                     : launch_v5<2>(bank, w, win, der, st, work, out, s);
+        if (rc) return rc;
+    } else if (kernel_gen() == 4) {
         rc = D <= 32 ? launch_v4<1>(bank, w, win, der, st, work, out, s)
                      : launch_v4<2>(bank, w, win, der, st, work, out, s);
         if (rc) return rc;
