@@ -178,6 +178,9 @@ typedef struct fate_derived {
                                        the full-hit row (stage part 0); valid under
                                        FATE_BANK_UNIFORM_SPEED (costs.py:257, :404-405) */
     int32_t* inst_qgroups;          /* [n_instances] 1 if any query has a prefix group */
+    double* tail_sum;               /* [n_stages*(n_models+1)] full tail value per
+                                       (stage, displacement class) when no level has a
+                                       locality op (costs.py:281-352) */
     double* tail_static;            /* [n_stages*levels*(n_models+1)] affinity chain per
                                        (stage, level, displacement class) with no locality
                                        op applied (costs.py:307-331) */

@@ -117,7 +117,8 @@ __device__ __forceinline__ double qc_value(long long stage_part, long long query
                                            double pcoef, double pscale, double decode,
                                            double cplx, double speed) {
     double prefill = (double)(stage_part + query_part) / 1000.0 * pcoef * pscale;
-    return (prefill + decode) * cplx / speed;
+    const double x = (prefill + decode) * cplx;
+    return speed == 1.0 ? x : x / speed;  // x / 1.0 == x exactly
 }
 
 struct ItemSmem {
@@ -680,6 +681,13 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
                                                   s>>>(*bank, *w, *win, out->tail_static);
                 g_launches++;
                 if ((rc = cuda_status("fate_prepare_tail_static_kernel"))) return rc;
+                if (out->tail_sum) {
+                    const long long ns = (long long)bank->n_stages * (bank->n_models + 1);
+                    fate_prepare_tail_sum_kernel<<<(unsigned)((ns + threads - 1) / threads),
+                                                   threads, 0, s>>>(*bank, *w, *win, *out);
+                    g_launches++;
+                    if ((rc = cuda_status("fate_prepare_tail_sum_kernel"))) return rc;
+                }
             }
         }
     }

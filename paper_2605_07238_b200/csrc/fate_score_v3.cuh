@@ -161,6 +161,28 @@ __global__ void fate_prepare_tail_static_kernel(fate_bank b, fate_weights w, fat
     tail_static[t] = aff;
 }
 
+// Prologue: full tail per (stage, displacement class) from the static level
+// chains and the demand table, accumulated level by level in the reference
+// order (costs.py:296-351).
+__global__ void fate_prepare_tail_sum_kernel(fate_bank b, fate_weights w, fate_windows win,
+                                             fate_derived der) {
+    const int M1 = b.n_models + 1;
+    const int LV = win.levels;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)b.n_stages * M1) return;
+    const int c = (int)(t % M1);
+    const long long v = t / M1;
+    double total = 0.0;
+    for (int l = 0; l < LV; ++l) {
+        const long long vl = v * LV + l;
+        const long long n = win.ptr[vl + 1] - win.ptr[vl];
+        if (n == 0) continue;
+        const double aff = der.tail_static[vl * M1 + c];
+        total += w.gamma_pow[l + 1] * (aff / (double)n + w.demand_coeff * der.demand[vl]);
+    }
+    der.tail_sum[t] = total;
+}
+
 template <int G>
 __global__ void __launch_bounds__(128) fate_score_v3_kernel(fate_bank b, fate_weights w,
                                                             fate_windows win, fate_derived der,

@@ -139,43 +139,34 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v5_kernel(fate_bank b, f
     it.dev_row0 = (long long)s * D;
     it.cap4 = st.kappa_cap * 4;
 
-    // ---- prefetch: horizon-level metadata and located-parent flags ---------------------------
-    int nb[V5_PLV];
-    double tstat[V5_PLV][DPL], dem[V5_PLV];
-    bool walk[V5_PLV];
+    // ---- prefetch: located-parent flag per horizon level and the static full tail --------
     int res0[DPL];
     bool live[DPL];
+    double tail_full[DPL];
 #pragma unroll
     for (int j = 0; j < DPL; ++j) {
         live[j] = t + 32 * j < D;
         res0[j] = live[j] ? st.residency[it.dev_row0 + t + 32 * j] : -1;
+        tail_full[j] = 0.0;
     }
     const bool do_tail = H > 1;
+    unsigned walk_m = 0u;  // bit l: level l has a locality op (needs the op-list walk)
+    if (do_tail) {
+        const double* row = der.tail_sum + (size_t)v * M1;
 #pragma unroll
-    for (int l = 0; l < V5_PLV; ++l) {
-        nb[l] = 0;
-        walk[l] = false;
-        dem[l] = 0.0;
-#pragma unroll
-        for (int j = 0; j < DPL; ++j) tstat[l][j] = 0.0;
-        if (do_tail && l < LV) {
-            const long long vl = (long long)v * LV + l;
-            nb[l] = (int)(win.ptr[vl + 1] - win.ptr[vl]);
-            dem[l] = der.demand[vl];
-            const double* row = der.tail_static + vl * M1;
-#pragma unroll
-            for (int j = 0; j < DPL; ++j) {
-                const int r = res0[j];
-                const int c = (r != -1 && r != m && r < b.n_models) ? 1 + r : 0;
-                tstat[l][j] = row[c];
-            }
-            bool located = false;
-            if (!no_loc) {
+        for (int j = 0; j < DPL; ++j) {
+            const int r = res0[j];
+            tail_full[j] = row[(r != -1 && r != m && r < b.n_models) ? 1 + r : 0];
+        }
+        if (!no_loc) {
+            for (int l = 0; l < LV; ++l) {
+                const long long vl = (long long)v * LV + l;
                 const long long w1 = win.wpar_ptr[vl + 1];
+                bool located = false;
                 for (long long i = win.wpar_ptr[vl] + t; i < w1; i += 32)
                     located |= loc_row[win.wpar_idx[i]] >= 0;
+                if (__any_sync(FULL, located)) walk_m |= 1u << (l < 31 ? l : 31);
             }
-            walk[l] = __any_sync(FULL, located);
         }
     }
     {
@@ -402,42 +393,24 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v5_kernel(fate_bank b, f
         tail[j] = 0.0;
         dmc[j] = (live[j] && res0[j] != -1 && res0[j] != m && res0[j] < b.n_models) ? res0[j] : -1;
     }
-    if (do_tail) {
+    if (do_tail && walk_m == 0u) {
+        // no locality op anywhere in the horizon: the whole tail is static
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) tail[j] = tail_full[j];
+    } else if (do_tail) {
         for (int l = 0; l < LV; ++l) {
             const long long vl = (long long)v * LV + l;
-            double aff[DPL], dml;
-            bool wl;
-            int n_b;
-            if (l < V5_PLV) {
-                // select chains keep the prefetched arrays in registers
-                n_b = nb[0]; dml = dem[0]; wl = walk[0];
-#pragma unroll
-                for (int j = 0; j < DPL; ++j) aff[j] = tstat[0][j];
-#pragma unroll
-                for (int c = 1; c < V5_PLV; ++c) {
-                    if (l == c) {
-                        n_b = nb[c]; dml = dem[c]; wl = walk[c];
-#pragma unroll
-                        for (int j = 0; j < DPL; ++j) aff[j] = tstat[c][j];
-                    }
-                }
-            } else {
-                n_b = (int)(win.ptr[vl + 1] - win.ptr[vl]);
-                dml = der.demand[vl];
+            const long long lo = win.ptr[vl];
+            const int n_b = (int)(win.ptr[vl + 1] - lo);
+            if (n_b == 0) continue;
+            const double dml = der.demand[vl];
+            double aff[DPL];
+            const bool wl = (walk_m >> (l < 31 ? l : 31)) & 1u;
+            if (!wl) {
                 const double* row = der.tail_static + vl * M1;
 #pragma unroll
                 for (int j = 0; j < DPL; ++j) aff[j] = row[1 + dmc[j]];
-                bool located = false;
-                if (!no_loc) {
-                    const long long w1 = win.wpar_ptr[vl + 1];
-                    for (long long i = win.wpar_ptr[vl] + t; i < w1; i += 32)
-                        located |= loc_row[win.wpar_idx[i]] >= 0;
-                }
-                wl = __any_sync(FULL, located);
-            }
-            if (n_b == 0) continue;
-            const long long lo = wl ? win.ptr[vl] : 0;
-            if (wl) {
+            } else {
                 int base = 0;
                 for (int j0 = 0; j0 < n_b; j0 += 32) {
                     const int jx = j0 + t;
@@ -564,7 +537,8 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v5_kernel(fate_bank b, f
         const double wait = py_max0(fr[j] - clock);
         const double sw = V.sw[d];
         const double tr = V.tr[d];
-        const double colo = pa1 > pa0 ? (double)hit[j] / (double)(pa1 - pa0) : 0.0;
+        // 0 / n == +0.0 exactly: divide only when a parent is co-located
+        const double colo = (pa1 > pa0 && hit[j] > 0) ? (double)hit[j] / (double)(pa1 - pa0) : 0.0;
 
         // prefix_overlap_thousands (costs.py:127-145), integer-exact
         long long tokens = 0;
@@ -581,7 +555,8 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v5_kernel(fate_bank b, f
                 tokens += c < qp ? c : qp;
             }
         }
-        const double prefix = w.kappa_prefix * ((double)tokens / 1000.0) * w.prefix_x;
+        const double prefix =
+            w.kappa_prefix * (tokens == 0 ? 0.0 : (double)tokens / 1000.0) * w.prefix_x;
 
         // _parallel_benefit (costs.py:181-201)
         const double full_total = sw + tr + here[j];
@@ -643,7 +618,10 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v5_kernel(fate_bank b, f
             const double overhead = w.shard_overhead_frac * bb;
             const double tr_m = no_loc ? 0.0 : tr;
             for (int k = 1; k < bound; ++k) {
-                const double reduction = bb / (double)k - hv / (double)(k + 1);
+                // x / 1 == x and x / 2 == x * 0.5 exactly (both correctly rounded x/2)
+                const double q1 = k == 1 ? bb : bb / (double)k;
+                const double q2 = k == 1 ? hv * 0.5 : hv / (double)(k + 1);
+                const double reduction = q1 - q2;
                 psi[(long long)k * D + d] = w.lambda_r * (reduction - overhead) -
                                             w.lambda_q * wait - w.lambda_s * sw * w.state_scale -
                                             w.lambda_tr * (tr_m + split) * w.locality_scale;

@@ -211,6 +211,7 @@ class DeviceBank:
         self.row_sums = torch.empty(max(n * 6, 1), **f64)
         self.inst_qgroups = torch.empty(max(packed.scalars["n_instances"], 1), dtype=torch.int32,
                                         device=self.device)
+        self.tail_sum = torch.empty(max(n * (packed.scalars["n_models"] + 1), 1), **f64)
         n_static = n * self.levels * (packed.scalars["n_models"] + 1)
         self.tail_static = torch.empty(max(n_static, 1), **f64)
         self.cder = abi.FateDerived(mean_base=self.mean_base.data_ptr(),
@@ -220,6 +221,7 @@ class DeviceBank:
                                     edge_term=self.edge_term.data_ptr(),
                                     row_sums=self.row_sums.data_ptr(),
                                     inst_qgroups=self.inst_qgroups.data_ptr(),
+                                    tail_sum=self.tail_sum.data_ptr(),
                                     tail_static=self.tail_static.data_ptr())
         s = stream or torch.cuda.current_stream(self.device)
         _check(L.fate_prepare(C.byref(self.cbank), C.byref(self.cweights), C.byref(self.cwin),
