@@ -138,6 +138,9 @@ typedef struct fate_state {
     const int32_t* scen_inst;       /* [S] instance of the scenario */
     const double* scen_clock;       /* [S] */
     const int64_t* scen_loc_off;    /* [S] offset of the instance-local loc row */
+    const int32_t* scen_done_level; /* [S] max level of a stage with a located output
+                                       (-1 if none): window parents above it cannot be
+                                       located, so their gather is skipped */
     const int32_t* loc;             /* output_device(u) as device index, -1 = None */
     const int32_t* residency;       /* [S*D] model id, -1 = None */
     const double* dev_free;         /* [S*D] device_free */
@@ -164,6 +167,8 @@ typedef struct fate_windows {
     const int32_t* idx;             /* [ptr[end]] global stage indices */
     const int64_t* wpar_ptr;        /* [n_stages*levels+1] window parents per (v, l) */
     const int32_t* wpar_idx;        /* distinct parents != v of the bucket, ascending */
+    const int32_t* wpar_minlvl;     /* [n_stages*levels] min level of those parents
+                                       (INT32_MAX if none) */
 } fate_windows;
 
 /* Static per-(bank, weights) tables produced by fate_prepare. */

@@ -34,8 +34,11 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
+        try:  # incremental: rebuilds when fate_oracle.c or include/fate.h changed
             build()
+        except (OSError, subprocess.CalledProcessError):
+            if not os.path.exists(_LIB_PATH):
+                raise
         L = C.CDLL(_LIB_PATH)
         L.oracle_score.restype = C.c_int
         L.oracle_score.argtypes = [C.c_void_p] * 5 + [C.c_int]

@@ -44,8 +44,8 @@ class FateBank(C.Structure):
                 + [(n, _p) for n in BANK_PTRS])
 
 
-STATE_PTRS = ("scen_inst", "scen_clock", "scen_loc_off", "loc", "residency", "dev_free",
-              "kappa_n", "kappa")
+STATE_PTRS = ("scen_inst", "scen_clock", "scen_loc_off", "scen_done_level", "loc", "residency",
+              "dev_free", "kappa_n", "kappa")
 
 
 class FateState(C.Structure):
@@ -59,7 +59,7 @@ class FateWork(C.Structure):
 
 class FateWindows(C.Structure):
     _fields_ = [("levels", C.c_int32), ("max_level_ops", C.c_int32), ("ptr", _p), ("idx", _p),
-                ("wpar_ptr", _p), ("wpar_idx", _p)]
+                ("wpar_ptr", _p), ("wpar_idx", _p), ("wpar_minlvl", _p)]
 
 
 class FateDerived(C.Structure):

@@ -159,8 +159,12 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v5_kernel(fate_bank b, f
             tail_full[j] = row[(r != -1 && r != m && r < b.n_models) ? 1 + r : 0];
         }
         if (!no_loc) {
+            // a window parent above the scenario's highest located stage cannot be
+            // located: levels whose parents all lie above it need no gather
+            const int done_lvl = st.scen_done_level[s];
             for (int l = 0; l < LV; ++l) {
                 const long long vl = (long long)v * LV + l;
+                if (win.wpar_minlvl[vl] > done_lvl) continue;
                 const long long w1 = win.wpar_ptr[vl + 1];
                 bool located = false;
                 for (long long i = win.wpar_ptr[vl] + t; i < w1; i += 32)
@@ -169,6 +173,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v5_kernel(fate_bank b, f
             }
         }
     }
+    const double rsum = t < 6 ? der.row_sums[(size_t)v * 6 + t] : 0.0;  // static-class sums
     {
         const int ri = b.st_role[v];
         it.pcoef = m >= 0 ? b.model_prefill[m] : 1.0;
@@ -304,20 +309,15 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v5_kernel(fate_bank b, f
         }
         V.cslot[dv[j]] = slot;
     }
-    if (t == 0) {
-        const double* z = der.row_sums + (size_t)v * 6;
-#pragma unroll
-        for (int si = 0; si < 2; ++si) {
-            if (!(si == 0 ? am : bm)) continue;
-            const double* zz = z + 3 * si;
-            V.aware[si] = zz[0];
-            if (kb == 2) {
-                V.shard[(si * 2 + 0) * V5_KT + 0] = zz[1];
-                V.shard[(si * 2 + 0) * V5_KT + 1] = zz[2];
-            }
-            if (ki == 2 && ki != kb) {
-                V.shard[(si * 2 + 1) * V5_KT + 0] = zz[1];
-                V.shard[(si * 2 + 1) * V5_KT + 1] = zz[2];
+    if (t < 6) {
+        // lane t holds row_sums[v][t]: class si = t / 3, entry e = t % 3 (full, shard 0, 1)
+        const int si = t / 3, e = t - 3 * si;
+        if (si == 0 ? am != 0ull : bm != 0ull) {
+            if (e == 0) {
+                V.aware[si] = rsum;
+            } else {
+                if (kb == 2) V.shard[(si * 2 + 0) * V5_KT + (e - 1)] = rsum;
+                if (ki == 2 && ki != kb) V.shard[(si * 2 + 1) * V5_KT + (e - 1)] = rsum;
             }
         }
     }

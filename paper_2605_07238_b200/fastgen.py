@@ -170,8 +170,12 @@ def synth_batch(cfg, n_inst: int, seed0: int, scen0: int, depth: int, width: int
                       group_index={f"pg:{m}": i for i, m in enumerate(catalog)}, arrays=arrays,
                       scalars=scalars, instances=[None] * n_inst, stage_ids=[sids] * n_inst,
                       stage_index=[sindex] * n_inst, inst_stage_off=arrays["inst_stage_off"])
+    loc2 = got["loc"].reshape(n_inst, V)
+    lvl2 = arrays["st_level"].reshape(n_inst, V)
+    done = np.where(loc2 >= 0, lvl2, -1).max(axis=1).astype(np.int32)
     st_arrays = dict(scen_inst=np.arange(n_inst, dtype=np.int32), scen_clock=clock,
-                     scen_loc_off=(np.arange(n_inst, dtype=np.int64) * V), loc=got["loc"],
+                     scen_loc_off=(np.arange(n_inst, dtype=np.int64) * V),
+                     scen_done_level=done, loc=got["loc"],
                      residency=got["residency"], dev_free=free, kappa_n=got["kappa_n"],
                      kappa=got["kappa"])
     states = PackedStates(arrays=st_arrays, n_scenarios=n_inst, kappa_cap=cap)

@@ -314,7 +314,9 @@ def pack_states(bank: PackedBank, scenarios, kappa_cap: int | None = None) -> Pa
     kap_n = np.zeros(n_s * n_dev, dtype=np.int32)
     kap = np.zeros((n_s * n_dev, cap, 4), dtype=np.int32)
     locs = []
+    done_level = np.full(n_s, -1, dtype=np.int32)
     off = 0
+    lvl_all = bank.arrays["st_level"]
     for s, (ii, st) in enumerate(scenarios):
         scen_inst[s] = ii
         clock[s] = float(st.clock)
@@ -326,6 +328,9 @@ def pack_states(bank: PackedBank, scenarios, kappa_cap: int | None = None) -> Pa
             if dev is not None and sid in sindex:
                 row[sindex[sid]] = dev_index[dev]
         locs.append(row)
+        if np.any(row >= 0):
+            g0 = int(bank.inst_stage_off[ii])
+            done_level[s] = int(lvl_all[g0: g0 + len(sindex)][row >= 0].max())
         off += len(sindex)
         base = s * n_dev
         for dev, di in dev_index.items():
@@ -339,7 +344,7 @@ def pack_states(bank: PackedBank, scenarios, kappa_cap: int | None = None) -> Pa
                 kap[base + di, k, 1] = int(ent.tokens)
                 kap[base + di, k, 2] = bank.model_id(ent.model)
     arrays = dict(
-        scen_inst=scen_inst, scen_clock=clock, scen_loc_off=loc_off,
+        scen_inst=scen_inst, scen_clock=clock, scen_loc_off=loc_off, scen_done_level=done_level,
         loc=np.concatenate(locs) if locs else np.zeros(1, dtype=np.int32),
         residency=residency, dev_free=free, kappa_n=kap_n, kappa=kap.ravel(),
     )

@@ -122,6 +122,26 @@ def build_window_parents(packed: PackedBank, levels: int):
     return wptr, widx
 
 
+def window_parent_min_level(packed: PackedBank, levels: int) -> np.ndarray:
+    """Per (stage, level): the lowest level among the window parents
+    (INT32_MAX when the list is empty)."""
+    key = ("wpar_min", levels)
+    if key in packed.windows:
+        return packed.windows[key]
+    n = packed.n_stages * levels
+    out = np.full(max(n, 1), np.iinfo(np.int32).max, dtype=np.int32)
+    if n:
+        wptr, widx = build_window_parents(packed, levels)
+        cnt = (wptr[1:] - wptr[:-1])
+        if int(wptr[-1]) > 0:
+            lv = packed.arrays["st_level"][widx[: int(wptr[-1])]]
+            nz = cnt > 0
+            starts = wptr[:-1][nz]
+            out[:n][nz] = np.minimum.reduceat(lv, starts)
+    packed.windows[key] = out
+    return out
+
+
 def max_level_ops(packed: PackedBank, levels: int) -> int:
     """Largest per-(stage, level) op count of the tail: sum over the bucket of
     (model op + prefix op + parent edges); sizes the kernel's op buffer."""
@@ -196,11 +216,14 @@ class DeviceBank:
         wptr, widx = build_window_parents(packed, self.levels)
         self.wpar_ptr = _to_dev(torch, wptr, self.device)
         self.wpar_idx = _to_dev(torch, widx, self.device)
+        self.wpar_minlvl = _to_dev(torch, window_parent_min_level(packed, self.levels),
+                                   self.device)
         self.cwin = abi.FateWindows(levels=self.levels,
                                     max_level_ops=max_level_ops(packed, self.levels),
                                     ptr=self.win_ptr.data_ptr(), idx=self.win_idx.data_ptr(),
                                     wpar_ptr=self.wpar_ptr.data_ptr(),
-                                    wpar_idx=self.wpar_idx.data_ptr())
+                                    wpar_idx=self.wpar_idx.data_ptr(),
+                                    wpar_minlvl=self.wpar_minlvl.data_ptr())
         n, e = packed.n_stages, packed.scalars["n_edges"]
         f64 = dict(dtype=torch.float64, device=self.device)
         self.mean_base = torch.empty(max(n, 1), **f64)
@@ -344,6 +367,7 @@ class HostPipeline:
             p0 = int(work.psi_off[i0])
             p1 = int(work.psi_off[i1]) if i1 < n else work.n_psi
             sl = {"scen_inst": (s0, s1), "scen_clock": (s0, s1), "scen_loc_off": (s0, s1),
+                  "scen_done_level": (s0, s1),
                   "loc": (l0, l1), "residency": (s0 * D, s1 * D), "dev_free": (s0 * D, s1 * D),
                   "kappa_n": (s0 * D, s1 * D), "kappa": (s0 * D * cap4, s1 * D * cap4),
                   "w:scen": (i0, i1), "w:stage": (i0, i1), "w:psi_off": (i0, i1)}

@@ -333,5 +333,39 @@ def main():
         gen_sampled(a.parallel, a.quick)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--c5-assign" not in sys.argv:
     main()
+
+
+# ---------------------------------------------------------------------------
+# config 5 assignments (host solve on the reference's own cost matrix)
+# ---------------------------------------------------------------------------
+
+
+def _c5_assign(i):
+    from wfsched.costs import CostModel
+    from wfsched.model import ready_set
+
+    cfg = SC.config_c5()
+    rdag = RB.synth_generate(RB.SuiteSpec(kind="synthetic", depth=20, width=25, density=0.12,
+                                          seed=1000 + i, batch_size=16), cfg)
+    rinst = RB.make_instance(rdag, 16, 1000 + i)
+    st = SC.build_scenario(rinst, cfg, i, kit=reference_kit())
+    cm = CostModel(cfg.models, cfg.topology, cfg.weights)
+    front = set(ready_set(rinst.dag, st.completed))
+    prob = RP.build_problem(front, st, cm, rinst.dag)
+    sol = RP.solve_frontier(prob, budget_s=0.0)
+    return {"instance": i, "selected": [list(x) for x in sol.selected],
+            "objective": sol.objective.hex(), "n_candidates": len(prob.candidates)}
+
+
+def gen_c5_assign(parallel: int, n: int = 16):
+    with mp.get_context("fork").Pool(parallel) as pool:
+        res = pool.map(_c5_assign, list(range(n)), chunksize=1)
+    with open(os.path.join(HERE, "c5_assign.json"), "w") as fh:
+        json.dump({"budget_s": 0.0, "instances": res}, fh, indent=0, sort_keys=True)
+    print(f"c5_assign: {len(res)} instances")
+
+
+if __name__ == "__main__" and "--c5-assign" in sys.argv:
+    gen_c5_assign(os.cpu_count() or 4)

@@ -184,3 +184,41 @@ def check_c45_sampled(gpu: bool) -> int:
                 got = out[key][w * D: (w + 1) * D][cols].view(np.uint64).tolist()
                 assert got == it[key], (which, idx, it["stage"], key)
     return checked
+
+
+def check_c5_assign(gpu: bool) -> int:
+    """Config-5 assignments: the host solve (budget 0, deterministic greedy) on
+    the GPU/oracle cost matrix selects exactly what the reference's solve
+    selects on the reference's own cost matrix (tests/golden/c5_assign.json)."""
+    from paper_2605_07238_b200.wf.frontier import Candidate, FrontierProblem, solve_frontier
+
+    with open(os.path.join(G.GOLDEN, "c5_assign.json")) as fh:
+        golden = json.load(fh)
+    cfg = scenarios.config_c5()
+    n = 0
+    for g in golden["instances"]:
+        i = g["instance"]
+        inst = scenarios.c5_instance(i, cfg)
+        st = scenarios.build_scenario(inst, cfg, i)
+        bank = pack.pack_bank([inst], cfg.models, cfg.topology)
+        sids = scenarios.scenario_frontier(inst, st)
+        pst = pack.pack_states(bank, [(0, st)])
+        work = pack.make_work(bank, [(0, bank.global_index(0, s)) for s in sids], False)
+        if gpu:
+            from paper_2605_07238_b200 import runtime
+
+            psi = runtime.DeviceBank(bank, cfg.weights).score(pst, work, extras=False).psi
+            psi = psi.cpu().numpy()
+        else:
+            import oracle
+
+            psi = oracle.score(bank, pack.weights_record(cfg.weights), pst, work)["psi"]
+        cands = tuple(Candidate(*c) for c in pack.candidates_from_psi(bank, work, psi, 0))
+        assert len(cands) == g["n_candidates"]
+        prob = FrontierProblem(cands, {s: int(b) for s, b in zip(sids, work.bounds)},
+                               tuple(cfg.topology.device_ids))
+        sol = solve_frontier(prob, budget_s=golden["budget_s"])
+        assert [list(x) for x in sol.selected] == g["selected"], i
+        assert sol.objective.hex() == g["objective"], i
+        n += 1
+    return n

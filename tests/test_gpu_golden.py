@@ -69,3 +69,7 @@ def test_c2_suite_and_table1(scorer):
 
 def test_c45_sampled(scorer):
     GC.check_c45_sampled(gpu=True)
+
+
+def test_c5_assignments_budget0(scorer):
+    assert GC.check_c5_assign(gpu=True) == 16

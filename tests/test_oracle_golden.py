@@ -68,3 +68,7 @@ def test_replay_c2_and_table1():
                     reason="c45 golden not generated")
 def test_c45_sampled():
     assert GC.check_c45_sampled(gpu=False) > 2000
+
+
+def test_c5_assignments_budget0():
+    assert GC.check_c5_assign(gpu=False) == 16
