@@ -234,6 +234,77 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
  * benchmark's gpu_launches evidence). */
 int64_t fate_launch_count(void);
 
+/* ---- host-buffer entry (the reference-facing call with HOST objects) ------
+ * Replaces the per-wave Python loop of wfsched.planner.build_problem
+ * (planner.py:75-98) for a whole batch: state and work list in HOST memory
+ * (pin it for overlap), Psi / S / completion written to HOST memory.
+ *
+ * Host wire format: one fixed-size record per scenario (so any scenario range
+ * is ONE contiguous copy), the loc rows, and one 16-byte record per item.
+ * Scenario record, 16-byte aligned, FATE_SCEN_REC_BYTES(D, cap) bytes:
+ *   [0]          double  clock               (fate_state.scen_clock)
+ *   [8]          int64   loc_off             (fate_state.scen_loc_off)
+ *   [16]         int32   inst                (fate_state.scen_inst)
+ *   [20]         int32   done_level          (fate_state.scen_done_level)
+ *   [24]         int32   reserved[2]
+ *   [32]         int32   residency[D]
+ *   [32+4D]      int32   kappa_n[D]
+ *   [32+8D]      double  dev_free[D]
+ *   [32+16D]     int32   kappa[D*cap*4]      (group, tokens, model, 0) */
+#define FATE_SCEN_REC_BYTES(D, cap) (32 + 16 * (D) + 16 * (D) * (cap))
+
+typedef struct fate_item {
+    int32_t scen;
+    int32_t stage;                  /* global stage index */
+    int64_t psi_off;
+} fate_item;
+
+typedef struct fate_host_batch {
+    int32_t n_scenarios;
+    int32_t kappa_cap;
+    int64_t n_loc;
+    const void* scen_rec;           /* [S * FATE_SCEN_REC_BYTES(D, kappa_cap)] */
+    const int32_t* loc;             /* [n_loc]; scenario loc_off nondecreasing */
+    int32_t n_items;
+    int32_t reserved;
+    int64_t n_psi;                  /* entries of the Psi output */
+    const fate_item* items;         /* [n_items], scenario-major, psi_off increasing */
+} fate_host_batch;
+
+/* Opaque per-(process, GPU) handle: its streams, events and device
+ * workspaces.  Not thread-safe; one handle per caller thread. */
+typedef struct fate_pipeline fate_pipeline;
+
+int fate_pipeline_create(int device, int n_chunks, int n_streams, fate_pipeline** out);
+int fate_pipeline_destroy(fate_pipeline* p);
+
+/* Enqueue, per scenario-aligned chunk: H2D of its scenario records, loc rows
+ * and items (three copies) -> unpack into the fate_state / fate_work SoA ->
+ * fate_score -> D2H of Psi [, S, completion]; chunks round-robin on the
+ * handle's streams so copies in both directions overlap the scoring.  Ordered
+ * after the work already on `stream`; `stream` waits for all of it, so a
+ * stream synchronize (or an event recorded on it) marks the host outputs
+ * ready.  sched_host / completion_host may be NULL ([n_items*D] otherwise). */
+int fate_pipeline_score(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
+                        const fate_windows* win, const fate_derived* der,
+                        const fate_host_batch* hb, double* psi_host, double* sched_host,
+                        double* completion_host, void* stream);
+
+/* The same pipeline captured once into a CUDA graph (validation, chunking and
+ * workspace sizing happen here, on the host, once) and replayed per step:
+ * each replay re-reads the host inputs at the captured addresses and rewrites
+ * the host outputs, so callers refill the same pinned buffers between
+ * replays.  Re-capture when sizes or addresses change. */
+int fate_pipeline_capture(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
+                          const fate_windows* win, const fate_derived* der,
+                          const fate_host_batch* hb, double* psi_host, double* sched_host,
+                          double* completion_host);
+int fate_pipeline_replay(fate_pipeline* p, void* stream);
+
+/* Bytes moved host->device and device->host by the last fate_pipeline_score
+ * (or captured by fate_pipeline_capture: the bytes of one replay). */
+int fate_pipeline_bytes(const fate_pipeline* p, int64_t* h2d, int64_t* d2h);
+
 #ifdef __cplusplus
 }
 #endif

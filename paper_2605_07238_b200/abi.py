@@ -52,6 +52,12 @@ class FateState(C.Structure):
     _fields_ = [("n_scenarios", C.c_int32), ("kappa_cap", C.c_int32)] + [(n, _p) for n in STATE_PTRS]
 
 
+class FateHostBatch(C.Structure):
+    _fields_ = [("n_scenarios", C.c_int32), ("kappa_cap", C.c_int32), ("n_loc", C.c_int64),
+                ("scen_rec", _p), ("loc", _p), ("n_items", C.c_int32), ("reserved", C.c_int32),
+                ("n_psi", C.c_int64), ("items", _p)]
+
+
 class FateWork(C.Structure):
     _fields_ = [("n_items", C.c_int32), ("reserved", C.c_int32), ("scen", _p), ("stage", _p),
                 ("psi_off", _p)]

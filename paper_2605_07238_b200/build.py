@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfate.so")
 SOURCES = [os.path.join(CSRC, "fate_kernels.cu"), os.path.join(CSRC, "fate_host.cpp"),
-           os.path.join(CSRC, "fate_synth.cpp")]
+           os.path.join(CSRC, "fate_synth.cpp"), os.path.join(CSRC, "fate_pipeline.cpp")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-ffp-contract=off", "-I", INCLUDE]
@@ -37,7 +37,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = SOURCES + [os.path.join(INCLUDE, "fate.h"), __file__]
+    deps = SOURCES + [os.path.join(INCLUDE, "fate.h"), __file__] + [
+        os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     return any(os.path.getmtime(p) > t for p in deps)
 
 

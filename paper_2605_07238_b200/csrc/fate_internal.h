@@ -1,0 +1,24 @@
+// fate_internal.h -- shared by the library's translation units (not ABI).
+#ifndef FATE_INTERNAL_H
+#define FATE_INTERNAL_H
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <string>
+
+#include "fate.h"
+
+// Records msg as fate_last_error() and returns code.
+int fate_internal_fail(int code, const std::string& msg);
+
+// Library-wide kernel launch counter (fate_launch_count).
+long long fate_internal_launches();
+void fate_internal_count_launches(long long n);
+
+// Scatter wire-format scenario records [s0, s1) and items [i0, i1) (device
+// copies of fate_host_batch) into the fate_state / fate_work SoA of dst.
+int fate_internal_unpack(const void* rec, size_t rec_bytes, int s0, int s1, int D, int cap,
+                         const fate_item* items, int i0, int i1, const fate_state* dst,
+                         int32_t* w_scen, int32_t* w_stage, int64_t* w_psi_off, cudaStream_t s);
+
+#endif

@@ -39,6 +39,7 @@
 #include <vector>
 
 #include "fate.h"
+#include "fate_internal.h"
 
 namespace {
 
@@ -641,7 +642,63 @@ int check_weights(const fate_weights* w, const fate_windows* win) {
     return 0;
 }
 
+// Wire format -> SoA (fate_pipeline.cpp): blocks [0, n_s) scatter one scenario
+// record each (layout in fate.h), the remaining blocks scatter 128 items each.
+__global__ void fate_unpack_kernel(const unsigned char* __restrict__ rec, size_t rb, int s0,
+                                   int n_s, int D, int cap, const fate_item* __restrict__ items,
+                                   int i0, int n_i, fate_state dst, int32_t* w_scen,
+                                   int32_t* w_stage, int64_t* w_psi_off) {
+    if ((int)blockIdx.x < n_s) {
+        const int s = s0 + blockIdx.x;
+        const unsigned char* r = rec + rb * s;
+        if (threadIdx.x == 0) {
+            const_cast<double*>(dst.scen_clock)[s] = *reinterpret_cast<const double*>(r);
+            const_cast<int64_t*>(dst.scen_loc_off)[s] = *reinterpret_cast<const int64_t*>(r + 8);
+            const_cast<int32_t*>(dst.scen_inst)[s] = *reinterpret_cast<const int32_t*>(r + 16);
+            const_cast<int32_t*>(dst.scen_done_level)[s] = *reinterpret_cast<const int32_t*>(r + 20);
+        }
+        const int32_t* res = reinterpret_cast<const int32_t*>(r + 32);
+        const int32_t* kn = res + D;
+        const double* fr = reinterpret_cast<const double*>(r + 32 + 8 * D);
+        const int4* kap = reinterpret_cast<const int4*>(r + 32 + 16 * D);
+        const size_t row = (size_t)s * D;
+        for (int d = threadIdx.x; d < D; d += blockDim.x) {
+            const_cast<int32_t*>(dst.residency)[row + d] = res[d];
+            const_cast<int32_t*>(dst.kappa_n)[row + d] = kn[d];
+            const_cast<double*>(dst.dev_free)[row + d] = fr[d];
+        }
+        int4* kdst = reinterpret_cast<int4*>(const_cast<int32_t*>(dst.kappa)) + row * cap;
+        for (int k = threadIdx.x; k < D * cap; k += blockDim.x) kdst[k] = kap[k];
+    } else {
+        const int i = i0 + ((int)blockIdx.x - n_s) * blockDim.x + threadIdx.x;
+        if (i >= i0 + n_i) return;
+        const fate_item x = items[i];
+        w_scen[i] = x.scen;
+        w_stage[i] = x.stage;
+        w_psi_off[i] = x.psi_off;
+    }
+}
+
 }  // namespace
+
+int fate_internal_fail(int code, const std::string& msg) { return fail(code, msg); }
+
+long long fate_internal_launches() { return g_launches.load(); }
+
+void fate_internal_count_launches(long long n) { g_launches += n; }
+
+int fate_internal_unpack(const void* rec, size_t rec_bytes, int s0, int s1, int D, int cap,
+                         const fate_item* items, int i0, int i1, const fate_state* dst,
+                         int32_t* w_scen, int32_t* w_stage, int64_t* w_psi_off, cudaStream_t s) {
+    const int n_s = s1 - s0, n_i = i1 - i0;
+    const unsigned blocks = (unsigned)(n_s + (n_i + 127) / 128);
+    if (blocks == 0) return 0;
+    fate_unpack_kernel<<<blocks, 128, 0, s>>>(static_cast<const unsigned char*>(rec), rec_bytes,
+                                               s0, n_s, D, cap, items, i0, n_i, *dst, w_scen,
+                                               w_stage, w_psi_off);
+    g_launches++;
+    return cuda_status("fate_unpack_kernel");
+}
 
 // ---------------------------------------------------------------------------
 // C ABI

@@ -460,3 +460,52 @@ def compulsory_bytes(bank: PackedBank, work: WorkList, states: PackedStates, lev
     unit_out = 8 * slots.astype(np.float64) * n_dev
     total = float(np.sum(unit_in) + np.sum(unit_out))
     return int(math.floor(total + 0.5))
+
+
+# ---------------------------------------------------------------------------
+# host wire format of fate_pipeline_score (include/fate.h: fate_host_batch)
+# ---------------------------------------------------------------------------
+
+ITEM_DTYPE = np.dtype([("scen", "<i4"), ("stage", "<i4"), ("psi_off", "<i8")])
+
+
+def scen_rec_bytes(n_dev: int, cap: int) -> int:
+    """FATE_SCEN_REC_BYTES(D, cap)."""
+    return 32 + 16 * n_dev + 16 * n_dev * cap
+
+
+@dataclass
+class HostBatch:
+    rec: np.ndarray      # uint8 [S * rec_bytes]
+    loc: np.ndarray      # int32 [n_loc]
+    items: np.ndarray    # ITEM_DTYPE [W]
+    n_scenarios: int
+    kappa_cap: int
+    n_psi: int
+
+
+def host_batch(states: PackedStates, work: WorkList, n_dev: int) -> HostBatch:
+    """Pack scenario states + work list into the pipeline's wire format: one
+    fixed-size record per scenario, the loc rows, 16-byte items."""
+    a = states.arrays
+    S, cap = states.n_scenarios, states.kappa_cap
+    rb = scen_rec_bytes(n_dev, cap)
+    rec = np.zeros((S, rb), dtype=np.uint8)
+    rec[:, 0:8] = np.asarray(a["scen_clock"], dtype="<f8").reshape(S, 1).view(np.uint8)
+    rec[:, 8:16] = np.asarray(a["scen_loc_off"], dtype="<i8").reshape(S, 1).view(np.uint8)
+    rec[:, 16:20] = np.asarray(a["scen_inst"], dtype="<i4").reshape(S, 1).view(np.uint8)
+    rec[:, 20:24] = np.asarray(a["scen_done_level"], dtype="<i4").reshape(S, 1).view(np.uint8)
+    o = 32
+    for key, dt, width in (("residency", "<i4", n_dev), ("kappa_n", "<i4", n_dev),
+                           ("dev_free", "<f8", n_dev), ("kappa", "<i4", n_dev * cap * 4)):
+        arr = np.ascontiguousarray(np.asarray(a[key], dtype=dt).reshape(S, width))
+        nb = arr.shape[1] * arr.dtype.itemsize
+        rec[:, o:o + nb] = arr.view(np.uint8)
+        o += nb
+    assert o == rb
+    items = np.empty(work.n_items, dtype=ITEM_DTYPE)
+    items["scen"] = work.scen
+    items["stage"] = work.stage
+    items["psi_off"] = work.psi_off
+    return HostBatch(rec=rec.reshape(-1), loc=np.ascontiguousarray(a["loc"], dtype=np.int32),
+                     items=items, n_scenarios=S, kappa_cap=cap, n_psi=work.n_psi)

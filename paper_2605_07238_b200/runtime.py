@@ -58,6 +58,18 @@ def load_library():
     L.fate_prepare.argtypes = [C.c_void_p] * 5
     L.fate_score.restype = C.c_int
     L.fate_score.argtypes = [C.c_void_p] * 8
+    L.fate_pipeline_create.restype = C.c_int
+    L.fate_pipeline_create.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+    L.fate_pipeline_destroy.restype = C.c_int
+    L.fate_pipeline_destroy.argtypes = [C.c_void_p]
+    L.fate_pipeline_score.restype = C.c_int
+    L.fate_pipeline_score.argtypes = [C.c_void_p] * 10
+    L.fate_pipeline_capture.restype = C.c_int
+    L.fate_pipeline_capture.argtypes = [C.c_void_p] * 9
+    L.fate_pipeline_replay.restype = C.c_int
+    L.fate_pipeline_replay.argtypes = [C.c_void_p, C.c_void_p]
+    L.fate_pipeline_bytes.restype = C.c_int
+    L.fate_pipeline_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     if L.fate_abi_version() != 1:
         raise FateUnavailable("libfate.so ABI version mismatch")
     _lib = L
@@ -312,99 +324,90 @@ class DeviceWork:
 
 
 class HostPipeline:
-    """Reference-facing call with HOST buffers: each call copies the step's
-    scenario states and work list host->device from pinned memory, scores,
-    and copies Psi device->host into pinned memory.  The static bank stays
+    """Reference-facing call with HOST buffers (``fate_pipeline_score``): each
+    call copies the step's scenario states and work list host->device from
+    pinned memory (the wire format of ``fate_host_batch``: fixed-size scenario
+    records, loc rows, 16-byte items), scores, and copies Psi (and optionally
+    S / completion) device->host into pinned memory.  The static bank stays
     HBM-resident (uploaded once, like model weights).
 
-    The batch is split into ``n_chunks`` scenario-aligned chunks issued
-    round-robin on ``n_streams`` CUDA streams, so the H2D copy of chunk i+1,
-    the scoring of chunk i and the D2H copy of chunk i-1 overlap (copy engines
-    and SMs run concurrently).  Items must be scenario-major (as every work
-    list built by this package is)."""
+    The native pipeline cuts the batch into ``n_chunks`` scenario-aligned
+    chunks issued round-robin on ``n_streams`` CUDA streams, so the H2D copy
+    of chunk i+1, the scoring of chunk i and the D2H copy of chunk i-1 overlap
+    (copy engines and SMs run concurrently).  Items must be scenario-major (as
+    every work list built by this package is).
+
+    ``graph=True`` captures the whole pipeline once into a CUDA graph
+    (``fate_pipeline_capture``: validation, chunking and sizing happen once)
+    and ``run()`` replays it: one launch per step, no per-copy host work on
+    the critical path.  Refill ``h_rec`` / ``h_loc`` / ``h_items`` in place
+    between replays to score new inputs of the same shape."""
 
     def __init__(self, dbank: DeviceBank, states: PackedStates, work: WorkList,
-                 extras: bool = False, n_chunks: int = 8, n_streams: int = 3):
+                 extras: bool = False, n_chunks: int = 8, n_streams: int = 1,
+                 graph: bool = False):
+        from .pack import host_batch
+
         torch = dbank.torch
+        L = load_library()
         self.dbank = dbank
+        self.L = L
         D = dbank.packed.scalars["n_devices"]
-        cap4 = states.kappa_cap * 4
-        sc = np.asarray(work.scen)
-        if sc.size and np.any(np.diff(sc) < 0):
-            raise ValueError("HostPipeline needs a scenario-major work list")
-        if work.n_items and np.any(np.diff(work.psi_off) < 0):
-            raise ValueError("HostPipeline needs increasing psi offsets")
-        sa = states.arrays
-        self.host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
-                     for k, v in sa.items()}
-        for k in ("scen", "stage", "psi_off"):
-            self.host["w:" + k] = torch.from_numpy(
-                np.ascontiguousarray(getattr(work, k))).pin_memory()
-        self.dev = {k: torch.empty_like(v, device=dbank.device) for k, v in self.host.items()}
-        self.cstate = abi.fill_struct(
-            abi.FateState(), {"n_scenarios": states.n_scenarios, "kappa_cap": states.kappa_cap},
-            {k: self.dev[k].data_ptr() for k in abi.STATE_PTRS})
-        self.out = dbank.alloc_out(work, extras=extras)
-        self.host_psi = torch.empty(self.out.psi.shape, dtype=torch.float64).pin_memory()
-        # scenario-aligned chunks
-        n = work.n_items
-        bounds = [0]
-        if n:
-            for c in range(1, n_chunks):
-                i = (n * c) // n_chunks
-                while 0 < i < n and sc[i] == sc[i - 1]:
-                    i += 1
-                if bounds[-1] < i < n:
-                    bounds.append(i)
-            bounds.append(n)
-        loc_off = np.asarray(sa["scen_loc_off"])
-        n_loc = sa["loc"].size
-        self.chunks = []
-        for i0, i1 in zip(bounds[:-1], bounds[1:]):
-            s0, s1 = int(sc[i0]), int(sc[i1 - 1]) + 1
-            l0 = int(loc_off[s0])
-            l1 = int(loc_off[s1]) if s1 < states.n_scenarios else n_loc
-            p0 = int(work.psi_off[i0])
-            p1 = int(work.psi_off[i1]) if i1 < n else work.n_psi
-            sl = {"scen_inst": (s0, s1), "scen_clock": (s0, s1), "scen_loc_off": (s0, s1),
-                  "scen_done_level": (s0, s1),
-                  "loc": (l0, l1), "residency": (s0 * D, s1 * D), "dev_free": (s0 * D, s1 * D),
-                  "kappa_n": (s0 * D, s1 * D), "kappa": (s0 * D * cap4, s1 * D * cap4),
-                  "w:scen": (i0, i1), "w:stage": (i0, i1), "w:psi_off": (i0, i1)}
-            cw = abi.fill_struct(abi.FateWork(), {"n_items": i1 - i0}, {
-                k: self.dev["w:" + k].data_ptr() + i0 * self.dev["w:" + k].element_size()
-                for k in ("scen", "stage", "psi_off")})
-            self.chunks.append((sl, cw, (p0, p1)))
-        self.streams = [torch.cuda.Stream(dbank.device) for _ in range(max(1, n_streams))]
-        self.h2d_bytes = sum(v.numel() * v.element_size() for v in self.host.values())
-        self.d2h_bytes = work.n_psi * 8
+        hb = host_batch(states, work, D)
+        pin = (lambda a: torch.from_numpy(a).pin_memory())
+        self.h_rec = pin(hb.rec)
+        self.h_loc = pin(hb.loc if hb.loc.size else np.zeros(1, np.int32))
+        self.h_items = pin(hb.items.view(np.uint8))
+        self.batch = abi.FateHostBatch(
+            n_scenarios=hb.n_scenarios, kappa_cap=hb.kappa_cap, n_loc=int(hb.loc.size),
+            scen_rec=self.h_rec.data_ptr(), loc=self.h_loc.data_ptr(), n_items=work.n_items,
+            n_psi=work.n_psi, items=self.h_items.data_ptr())
+        f64 = dict(dtype=torch.float64, pin_memory=True)
+        self.host_psi = torch.empty(max(work.n_psi, 1), **f64)
+        self.host_sched = torch.empty(max(work.n_items * D, 1), **f64) if extras else None
+        self.host_completion = torch.empty(max(work.n_items * D, 1), **f64) if extras else None
+        h = C.c_void_p()
+        dev = dbank.device.index if dbank.device.index is not None else torch.cuda.current_device()
+        _check(L.fate_pipeline_create(dev, n_chunks, n_streams, C.byref(h)),
+               "fate_pipeline_create")
+        self.handle = h
+        self.graph = False
+        if graph:
+            ptr = (lambda t: C.c_void_p(t.data_ptr()) if t is not None else None)
+            _check(L.fate_pipeline_capture(
+                self.handle, C.byref(dbank.cbank), C.byref(dbank.cweights), C.byref(dbank.cwin),
+                C.byref(dbank.cder), C.byref(self.batch), ptr(self.host_psi),
+                ptr(self.host_sched), ptr(self.host_completion)), "fate_pipeline_capture")
+            self.graph = True
+        self.run()  # sizes the workspaces; records the byte counts
+        torch.cuda.synchronize(dbank.device)
+        a, b = C.c_int64(0), C.c_int64(0)
+        _check(L.fate_pipeline_bytes(self.handle, C.byref(a), C.byref(b)), "fate_pipeline_bytes")
+        self.h2d_bytes, self.d2h_bytes = int(a.value), int(b.value)
 
     def run(self, stream=None):
         torch = self.dbank.torch
-        main = stream or torch.cuda.current_stream(self.dbank.device)
-        start = torch.cuda.Event()
-        start.record(main)
+        s = stream or torch.cuda.current_stream(self.dbank.device)
         d = self.dbank
-        L = load_library()
-        cout = abi.FateOut(psi=self.out.psi.data_ptr(),
-                           sched=self.out.sched.data_ptr() if self.out.sched is not None else None,
-                           tail=self.out.tail.data_ptr() if self.out.tail is not None else None,
-                           completion=(self.out.completion.data_ptr()
-                                       if self.out.completion is not None else None))
-        for c, (sl, cw, (p0, p1)) in enumerate(self.chunks):
-            s = self.streams[c % len(self.streams)]
-            s.wait_event(start)
-            with torch.cuda.stream(s):
-                for k, (a, b_) in sl.items():
-                    if b_ > a:
-                        self.dev[k][a:b_].copy_(self.host[k][a:b_], non_blocking=True)
-                _check(L.fate_score(C.byref(d.cbank), C.byref(d.cweights), C.byref(d.cwin),
-                                    C.byref(d.cder), C.byref(self.cstate), C.byref(cw),
-                                    C.byref(cout), C.c_void_p(s.cuda_stream)), "fate_score")
-                if p1 > p0:
-                    self.host_psi[p0:p1].copy_(self.out.psi[p0:p1], non_blocking=True)
-        for s in self.streams:
-            ev = torch.cuda.Event()
-            ev.record(s)
-            main.wait_event(ev)
+        if self.graph:
+            _check(self.L.fate_pipeline_replay(self.handle, C.c_void_p(s.cuda_stream)),
+                   "fate_pipeline_replay")
+            return self.host_psi
+        ptr = (lambda t: C.c_void_p(t.data_ptr()) if t is not None else None)
+        _check(self.L.fate_pipeline_score(
+            self.handle, C.byref(d.cbank), C.byref(d.cweights), C.byref(d.cwin),
+            C.byref(d.cder), C.byref(self.batch), ptr(self.host_psi),
+            ptr(self.host_sched), ptr(self.host_completion), C.c_void_p(s.cuda_stream)),
+            "fate_pipeline_score")
         return self.host_psi
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.L.fate_pipeline_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

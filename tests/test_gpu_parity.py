@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_2605_07238_b200 import runtime
+from paper_2605_07238_b200 import pack, runtime
 from paper_2605_07238_b200.wf.weights import AblationFlags
 
 from cases import ALL_ABLATIONS, bits, c4_case, c5_case, edge_case, small_case
@@ -84,15 +84,75 @@ def test_library_is_native():
 
 
 def test_host_pipeline_chunks_match_device_path():
-    """The pinned host-buffer call (chunked over 3 streams) returns exactly the
-    device-resident result."""
-    case = c5_case(n_inst=5)
-    dbank = runtime.DeviceBank(case.bank, case.weights)
-    want = dbank.score(case.states, case.work, extras=False).psi.cpu().numpy()[: case.work.n_psi]
-    pipe = runtime.HostPipeline(dbank, case.states, case.work, n_chunks=4, n_streams=3)
-    got = pipe.run()
+    """The pinned host-buffer call (native fate_pipeline_score, chunked over 3
+    streams) returns exactly the device-resident result, S and completion
+    included, and exactly the oracle."""
     import torch
 
+    case = c5_case(n_inst=5)
+    dbank = runtime.DeviceBank(case.bank, case.weights)
+    res = dbank.score(case.states, case.work, extras=True)
+    n = case.work.n_psi
+    for chunks, streams, graph in ((4, 3, False), (1, 1, False), (64, 2, False), (8, 1, True),
+                                   (3, 2, True)):
+        pipe = runtime.HostPipeline(dbank, case.states, case.work, extras=True,
+                                    n_chunks=chunks, n_streams=streams, graph=graph)
+        pipe.host_psi.fill_(0.0)
+        before = runtime.launch_count()
+        got = pipe.run()
+        torch.cuda.synchronize()
+        assert runtime.launch_count() > before
+        assert np.array_equal(bits(got.numpy()[:n]), bits(res.psi.cpu().numpy()[:n]))
+        m = case.work.n_items * case.bank.scalars["n_devices"]
+        assert np.array_equal(bits(pipe.host_sched.numpy()[:m]), bits(res.sched.cpu().numpy()[:m]))
+        assert np.array_equal(bits(pipe.host_completion.numpy()[:m]),
+                              bits(res.completion.cpu().numpy()[:m]))
+        assert pipe.d2h_bytes == 8 * n + 16 * m
+        pipe.close()
+    want = oracle.score(case.bank, case.wrec, case.states, case.work)["psi"]
+    assert np.array_equal(bits(got.numpy()[:n]), bits(want))
+
+
+def test_host_pipeline_graph_replays_fresh_inputs():
+    """A captured pipeline re-reads the pinned inputs on every replay."""
+    import torch
+
+    case = c5_case(n_inst=4)
+    dbank = runtime.DeviceBank(case.bank, case.weights)
+    pipe = runtime.HostPipeline(dbank, case.states, case.work, n_chunks=2, graph=True)
+    first = pipe.run().clone()
     torch.cuda.synchronize()
-    assert np.array_equal(bits(got.numpy()[: case.work.n_psi]), bits(want))
-    assert len(pipe.chunks) >= 2
+    # perturb every scenario clock in the pinned wire records, replay, compare to oracle
+    D = case.bank.scalars["n_devices"]
+    rb = pack.scen_rec_bytes(D, case.states.kappa_cap)
+    rec = pipe.h_rec.numpy().reshape(-1, rb)
+    clocks = rec[:, 0:8].copy().view("<f8").ravel() + 7.25
+    rec[:, 0:8] = clocks.reshape(-1, 1).view(np.uint8)
+    got = pipe.run()
+    torch.cuda.synchronize()
+    arrays = dict(case.states.arrays)
+    arrays["scen_clock"] = clocks
+    st2 = pack.PackedStates(arrays=arrays, n_scenarios=case.states.n_scenarios,
+                            kappa_cap=case.states.kappa_cap)
+    want = oracle.score(case.bank, case.wrec, st2, case.work)["psi"]
+    n = case.work.n_psi
+    assert np.array_equal(bits(got.numpy()[:n]), bits(want))
+    assert not np.array_equal(bits(got.numpy()[:n]), bits(first.numpy()[:n]))
+
+
+def test_host_pipeline_skips_scenarios_without_items():
+    """Scenarios no item reads are not copied; results still exact."""
+    import torch
+
+    case = c5_case(n_inst=6)
+    keep = np.isin(case.work.scen, [1, 4])
+    sub = pack.make_work(case.bank, zip(case.work.scen[keep].tolist(),
+                                        case.work.stage[keep].tolist()), False)
+    dbank = runtime.DeviceBank(case.bank, case.weights)
+    pipe = runtime.HostPipeline(dbank, case.states, sub, n_chunks=3, n_streams=2)
+    got = pipe.run()
+    torch.cuda.synchronize()
+    want = oracle.score(case.bank, case.wrec, case.states, sub)["psi"]
+    assert np.array_equal(bits(got.numpy()[: sub.n_psi]), bits(want))
+    full = sum(v.nbytes for v in case.states.arrays.values())
+    assert pipe.h2d_bytes < full

@@ -170,3 +170,41 @@ def test_scenario_generator_is_deterministic():
     assert a.parent_loc == b.parent_loc and a.device_free == b.device_free
     front = scenarios.scenario_frontier(inst, a)
     assert len(front) == 25
+
+
+def test_pipeline_rejects_bad_arguments_before_touching_cuda():
+    """fate_pipeline_create validates its sizes first (status < 0, no CUDA call)."""
+    if not os.path.exists(runtime.LIB_PATH):
+        pytest.skip("libfate.so not built")
+    L = runtime.load_library()
+    h = ctypes.c_void_p()
+    assert L.fate_pipeline_create(0, 0, 1, ctypes.byref(h)) == -1
+    assert L.fate_pipeline_create(0, 4, 0, ctypes.byref(h)) == -1
+    assert b"chunk" in L.fate_last_error()
+    assert L.fate_pipeline_destroy(None) == 0
+
+
+def test_host_batch_wire_format_round_trip():
+    """The scenario records follow fate.h's FATE_SCEN_REC_BYTES layout."""
+    case = c5_case(n_inst=3)
+    D = case.bank.scalars["n_devices"]
+    hb = pack.host_batch(case.states, case.work, D)
+    a, S, cap = case.states.arrays, case.states.n_scenarios, case.states.kappa_cap
+    rb = pack.scen_rec_bytes(D, cap)
+    assert rb % 16 == 0 and hb.rec.size == S * rb
+    rec = hb.rec.reshape(S, rb)
+    assert np.array_equal(rec[:, 0:8].copy().view("<f8").ravel(), a["scen_clock"])
+    assert np.array_equal(rec[:, 8:16].copy().view("<i8").ravel(), a["scen_loc_off"])
+    assert np.array_equal(rec[:, 16:20].copy().view("<i4").ravel(), a["scen_inst"])
+    assert np.array_equal(rec[:, 20:24].copy().view("<i4").ravel(), a["scen_done_level"])
+    o = 32
+    assert np.array_equal(rec[:, o:o + 4 * D].copy().view("<i4").ravel(), a["residency"])
+    o += 4 * D
+    assert np.array_equal(rec[:, o:o + 4 * D].copy().view("<i4").ravel(), a["kappa_n"])
+    o += 4 * D
+    assert np.array_equal(rec[:, o:o + 8 * D].copy().view("<f8").ravel(), a["dev_free"])
+    o += 8 * D
+    assert np.array_equal(rec[:, o:].copy().view("<i4").ravel(), np.ravel(a["kappa"]))
+    assert hb.items.itemsize == 16
+    assert np.array_equal(hb.items["stage"], case.work.stage)
+    assert np.array_equal(hb.items["psi_off"], case.work.psi_off)
