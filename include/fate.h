@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FATE_ABI_VERSION 1
+#define FATE_ABI_VERSION 2
 #define FATE_MAX_DEVICES 64
 #define FATE_MAX_HORIZON 32
 #define FATE_MAX_QUERIES 256
@@ -189,6 +189,14 @@ typedef struct fate_derived {
     double* tail_static;            /* [n_stages*levels*(n_models+1)] affinity chain per
                                        (stage, level, displacement class) with no locality
                                        op applied (costs.py:307-331) */
+    void* stage_rec;                /* [n_stages] 112-byte stage records (static per-stage
+                                       scalars of one item, csrc/fate_score_v6.cuh V6Stage) */
+    int64_t* tmpl_ptr;              /* [n_stages*levels+1] op-template offsets: exclusive
+                                       scan of fate_template_count's counts */
+    void* tmpl;                     /* [tmpl_ptr[end]] 16-byte op-template entries: per
+                                       (v, l) the reference's tail op sequence
+                                       (costs.py:307-348), edge entries resolved per
+                                       scenario by parent location */
 } fate_derived;
 
 /* Outputs.  psi: per item bound(v)*D entries, slot-major, NaN where the
@@ -223,6 +231,14 @@ int fate_window_parents_host(int32_t n_stages, int32_t levels, const int64_t* wi
  * locality terms).  Once per (bank, weights). */
 int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                  const fate_derived* out, void* stream);
+
+/* Device: op-template length of every (stage, level) window into counts
+ * [n_stages*levels] (device).  The caller scans it into fate_derived.tmpl_ptr,
+ * allocates fate_derived.tmpl (16 bytes per entry) and calls fate_prepare,
+ * which fills the templates and the stage records when those pointers are
+ * set.  Once per (bank, weights). */
+int fate_template_count(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+                        const fate_derived* der, int64_t* counts, void* stream);
 
 /* Device: score every work item.  Ψ for all slots and eligible devices, plus
  * the optional S / tail / completion matrices. */

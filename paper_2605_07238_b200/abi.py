@@ -70,7 +70,8 @@ class FateWindows(C.Structure):
 
 class FateDerived(C.Structure):
     _fields_ = [(n, _p) for n in ("mean_base", "demand", "split_penalty", "edge_sigma",
-                                  "edge_term", "row_sums", "inst_qgroups", "tail_sum", "tail_static")]
+                                  "edge_term", "row_sums", "inst_qgroups", "tail_sum", "tail_static",
+                                  "stage_rec", "tmpl_ptr", "tmpl")]
 
 
 class FateOut(C.Structure):

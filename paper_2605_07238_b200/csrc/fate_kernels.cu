@@ -530,6 +530,25 @@ __global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weigh
 #include "fate_score_v3.cuh"
 #include "fate_score_v4.cuh"
 #include "fate_score_v5.cuh"
+#include "fate_score_v6.cuh"
+
+template <int DPL, bool OVR, int MINB>
+int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+                 const fate_derived* der, const fate_state* st, const fate_work* work,
+                 const fate_out* out, cudaStream_t s) {
+    if (!der->stage_rec || (win->levels > 0 && (!der->tmpl_ptr || !der->tmpl)))
+        return fail(FATE_ENOTREADY, "v6 kernel needs stage records and op templates");
+    const V6Layout lay = v6_layout(bank->n_devices, bank->max_queries, win->max_level_ops);
+    const size_t smem = (size_t)lay.item_bytes * 4;
+    if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v6 shared-memory footprint too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fate_score_v6_kernel<DPL, OVR, MINB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const unsigned blocks = (unsigned)((work->n_items + 3) / 4);
+    fate_score_v6_kernel<DPL, OVR, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
+                                                                    *work, *out, lay);
+    return 0;
+}
 
 template <int DPL, int MINB>
 int launch_v5_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
@@ -585,6 +604,24 @@ int launch_v5(const fate_bank* bank, const fate_weights* w, const fate_windows* 
 }
 
 template <int DPL>
+int launch_v6(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+              const fate_derived* der, const fate_state* st, const fate_work* work,
+              const fate_out* out, cudaStream_t s) {
+    const bool ovr = bank->has_overrides != 0;
+    switch (v4_minb(DPL)) {
+        case 1:
+            return ovr ? launch_v6_mb<DPL, true, 1>(bank, w, win, der, st, work, out, s)
+                       : launch_v6_mb<DPL, false, 1>(bank, w, win, der, st, work, out, s);
+        case 6:
+            return ovr ? launch_v6_mb<DPL, true, 6>(bank, w, win, der, st, work, out, s)
+                       : launch_v6_mb<DPL, false, 6>(bank, w, win, der, st, work, out, s);
+        default:
+            return ovr ? launch_v6_mb<DPL, true, 8>(bank, w, win, der, st, work, out, s)
+                       : launch_v6_mb<DPL, false, 8>(bank, w, win, der, st, work, out, s);
+    }
+}
+
+template <int DPL>
 int launch_v4(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
               const fate_derived* der, const fate_state* st, const fate_work* work,
               const fate_out* out, cudaStream_t s) {
@@ -610,7 +647,9 @@ int launch_v3(const fate_bank* bank, const fate_weights* w, const fate_windows* 
     return 0;
 }
 
-// Kernel generation (A/B benchmarking only): FATE_SCORE_KERNEL=v1|v3|v4, default v5.
+// Kernel generation (A/B benchmarking only): FATE_SCORE_KERNEL=v1|v3|v4|v5,
+// default v6 (which needs the stage records and op templates; without them
+// the library falls back to v5, the previous production kernel).
 int kernel_gen() {
     static int v = -1;
     if (v < 0) {
@@ -618,7 +657,8 @@ int kernel_gen() {
         v = (e && strcmp(e, "v1") == 0)   ? 1
             : (e && strcmp(e, "v3") == 0) ? 3
             : (e && strcmp(e, "v4") == 0) ? 4
-                                          : 5;
+            : (e && strcmp(e, "v5") == 0) ? 5
+                                          : 6;
     }
     return v;
 }
@@ -726,12 +766,25 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
         fate_prepare_stage_kernel<<<blocks, threads, 0, s>>>(*bank, *w, *out);
         g_launches++;
         if ((rc = cuda_status("fate_prepare_stage_kernel"))) return rc;
+        if (out->stage_rec) {
+            if (!out->split_penalty || !out->inst_qgroups)
+                return fail(FATE_EINVAL, "stage records need split_penalty and inst_qgroups");
+            fate_prepare_stagerec_kernel<<<blocks, threads, 0, s>>>(*bank, *w, *out);
+            g_launches++;
+            if ((rc = cuda_status("fate_prepare_stagerec_kernel"))) return rc;
+        }
         const long long n = (long long)bank->n_stages * win->levels;
         if (n > 0) {
             fate_prepare_demand_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
                 *bank, *win, *out);
             g_launches++;
             if ((rc = cuda_status("fate_prepare_demand_kernel"))) return rc;
+            if (out->tmpl && out->tmpl_ptr) {
+                fate_template_fill_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0,
+                                            s>>>(*bank, *w, *win, *out);
+                g_launches++;
+                if ((rc = cuda_status("fate_template_fill_kernel"))) return rc;
+            }
             if (out->tail_static) {
                 const long long nt = n * (bank->n_models + 1);
                 fate_prepare_tail_static_kernel<<<(unsigned)((nt + threads - 1) / threads), threads, 0,
@@ -751,6 +804,22 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
     return 0;
 }
 
+int fate_template_count(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+                        const fate_derived* der, int64_t* counts, void* stream) {
+    int rc = check_bank(bank);
+    if (rc) return rc;
+    rc = check_weights(w, win);
+    if (rc) return rc;
+    if (!der || !counts) return fail(FATE_EINVAL, "derived/counts is NULL");
+    const long long n = (long long)bank->n_stages * win->levels;
+    if (n == 0) return 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    fate_template_count_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
+        *bank, *w, *win, *der, reinterpret_cast<long long*>(counts));
+    g_launches++;
+    return cuda_status("fate_template_count_kernel");
+}
+
 int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                const fate_derived* der, const fate_state* st, const fate_work* work,
                const fate_out* out, void* stream) {
@@ -766,7 +835,12 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int D = bank->n_devices;
     const size_t per_item = item_smem_bytes(D, bank->max_queries);
-    if (kernel_gen() == 5) {
+    const bool v6_ready = der->stage_rec && (win->levels == 0 || (der->tmpl_ptr && der->tmpl));
+    if (kernel_gen() == 6 && v6_ready) {
+        rc = D <= 32 ? launch_v6<1>(bank, w, win, der, st, work, out, s)
+                     : launch_v6<2>(bank, w, win, der, st, work, out, s);
+        if (rc) return rc;
+    } else if (kernel_gen() >= 5) {
         rc = D <= 32 ? launch_v5<1>(bank, w, win, der, st, work, out, s)
                      : launch_v5<2>(bank, w, win, der, st, work, out, s);
         if (rc) return rc;

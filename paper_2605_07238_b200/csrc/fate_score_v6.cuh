@@ -1,0 +1,765 @@
+// fate_score_v6.cuh -- warp-per-item scoring kernel, generation 6 (production).
+//
+// Included by fate_kernels.cu (inside its anonymous namespace), after v5.
+//
+// Same work decomposition and exactness argument as v5 (one warp per item =
+// (scenario, stage v); lane t owns devices t and t+32), with the per-item
+// instruction count and the dependent-load depth cut:
+//
+//  * stage record: every static per-stage scalar the item needs (model,
+//    shard bound, group, prompt, parent range, query range, instance offset,
+//    eligibility, bound, cost coefficients, switch value, split penalty,
+//    instance query-group flag) is one 112-byte record built by the prologue
+//    (fate_prepare_stagerec_kernel) and read with seven uniform 16-byte loads,
+//    instead of ~20 scalar loads two and three levels deep;
+//  * transfer without overrides: beta(L, d) == beta_default for every L != d
+//    when the topology has no transfer override (OVR = false), so v's parent
+//    walk multiplies by the constant instead of gathering beta rows;
+//  * tail op lists from static templates: per (v, level) the prologue lays out
+//    the reference's op sequence (costs.py:307-348: per descendant x, its
+//    model op, its prefix op, then one entry per parent edge of x other than
+//    v).  Model/prefix entries are final; an edge entry carries its parent
+//    index and is kept iff that parent is located in the scenario -- so a
+//    level's op list is built with one coalesced 16-byte load and one loc
+//    gather per 32 entries plus a ballot compaction, no nested parent loops;
+//  * op walk with predicated adds (inline PTX: two predicate-combining setp
+//    and one predicated add.rn.f64 per device slot).  Skipping an op equals
+//    adding +0.0 exactly because the chain starts at +0.0 and never becomes
+//    -0.0 in round-to-nearest (v5's argument), so this is v5's chain bit for
+//    bit;
+//  * shared-memory layout offsets computed once on the host (V6Layout).
+
+constexpr int V6_KT = 4;               // shard counts k <= V6_KT: shard sums tabulated
+constexpr int V6_RCAP = 8;             // dynamic classes with a shared-memory row
+constexpr int V6_SLOTS = V6_RCAP + 2;  // table slots: 0 = static A, 1 = static B, 2+ = rows
+constexpr int V6_KEY_ALWAYS = 999;     // op applied on every device (same-model, prefix)
+constexpr int V6_KEY_MODEL = 1000;     // op key >= this: displacement op of model key-1000
+constexpr int V6_KEY_SIGMA = 2000;     // OVR edge op: key-2000 = location, val = sigma
+
+// stage record flags
+constexpr int V6_CACHE_REUSE = 1;  // cache_reuse and a stage group
+constexpr int V6_QGROUPS = 2;      // the instance has queries with prefix groups
+
+struct __align__(16) V6Stage {
+    int m, R, gv, Pv;              // model (-1 None), shard bound R(v), group (-1), prompt
+    int pa0, pa1, q0, nq;          // parent CSR range, query range
+    int stage_off, flags, bound, n_elig;  // instance's first stage, V6_*, slots, |A(v)|
+    unsigned long long elig;       // eligible-device mask
+    int role, pad;
+    double pcoef, pscale;          // prefill coeff (1.0 without model), role prefill scale
+    double decode, cplx;           // out * decode coeff * decode scale, role complexity
+    double swv, split;             // switch cost if switching, slot>=1 split penalty
+};
+static_assert(sizeof(V6Stage) == 112, "V6Stage layout");
+
+struct __align__(16) V6Op {
+    double val;  // op value (edge entry: -edge_term, or sigma under OVR)
+    int pp;      // edge entry: parent stage (global index); -1 = static op
+    int key;     // static op key (V6_KEY_ALWAYS / V6_KEY_MODEL + mx)
+};
+static_assert(sizeof(V6Op) == 16, "V6Op layout");
+
+// Byte offsets of one item's shared-memory slice (host-computed).
+struct V6Layout {
+    int item_bytes;
+    int rows, shard, aware, sw, tr, opval, opkey, key, cslot, rowdev;
+};
+
+inline V6Layout v6_layout(int D, int Bmax, int ops_cap) {
+    V6Layout L{};
+    int o = 0;
+    const auto take = [&](int n, int sz) {
+        const int at = o;
+        o += n * sz;
+        o = (o + 15) & ~15;
+        return at;
+    };
+    L.rows = take(V6_RCAP * Bmax, 8);
+    L.shard = take(V6_SLOTS * 2 * V6_KT, 8);
+    L.aware = take(V6_SLOTS, 8);
+    L.sw = take(D, 8);
+    L.tr = take(D, 8);
+    L.opval = take(ops_cap > 0 ? ops_cap : 1, 8);
+    L.opkey = take(ops_cap > 0 ? ops_cap : 1, 4);
+    L.key = take(D, 4);
+    L.cslot = take(D, 4);
+    L.rowdev = take(V6_RCAP, 4);
+    L.item_bytes = o;
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+// prologue
+// ---------------------------------------------------------------------------
+
+// One thread per stage: the stage record (after fate_prepare_stage_kernel,
+// which produced split_penalty and inst_qgroups).
+__global__ void fate_prepare_stagerec_kernel(fate_bank b, fate_weights w, fate_derived der) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= b.n_stages) return;
+    V6Stage r;
+    const int inst = b.st_inst[g];
+    r.m = b.st_model[g];
+    r.R = b.st_shard[g];
+    r.gv = b.st_group[g];
+    r.Pv = b.st_prompt[g];
+    r.pa0 = b.par_ptr[g];
+    r.pa1 = b.par_ptr[g + 1];
+    r.q0 = b.inst_query_off[inst];
+    r.nq = b.inst_n_queries[inst];
+    r.stage_off = b.inst_stage_off[inst];
+    r.flags = (((b.st_flags[g] & FATE_STAGE_CACHE_REUSE) && r.gv != -1) ? V6_CACHE_REUSE : 0) |
+              (der.inst_qgroups[inst] ? V6_QGROUPS : 0);
+    r.elig = b.st_elig[g];
+    r.n_elig = __popcll(r.elig);
+    r.bound = (w.ablation & FATE_NO_SHARD) ? 1 : (r.R < r.n_elig ? r.R : r.n_elig);
+    r.role = b.st_role[g];
+    r.pad = 0;
+    const int ri = r.role;
+    r.pcoef = r.m >= 0 ? b.model_prefill[r.m] : 1.0;
+    const double dcoef = r.m >= 0 ? b.model_decode[r.m] : 0.0;
+    r.decode = (double)b.st_out[g] * dcoef * b.role_decode[ri];
+    r.pscale = b.role_prefill[ri];
+    r.cplx = b.role_cplx[ri];
+    r.swv = r.m >= 0 ? b.model_switch[r.m] * w.switch_x : 0.0;
+    r.split = der.split_penalty[g];
+    reinterpret_cast<V6Stage*>(der.stage_rec)[g] = r;
+}
+
+// Thread per (stage v, level l): length of the op template of the level
+// (model op + prefix op + parent edges other than v, per descendant).
+__device__ __forceinline__ long long v6_template_walk(const fate_bank& b, const fate_weights& w,
+                                                      const fate_windows& win,
+                                                      const fate_derived& der, long long vl,
+                                                      V6Op* out) {
+    const int LV = win.levels;
+    const int v = (int)(vl / LV);
+    const bool no_loc = w.ablation & FATE_NO_LOCALITY;
+    const bool no_pre = w.ablation & FATE_NO_PREFIX;
+    const bool no_same = w.ablation & FATE_NO_SAME_MODEL;
+    const int mv = b.st_model[v], gv = b.st_group[v], Pv = b.st_prompt[v];
+    long long n = 0;
+    for (long long i = win.ptr[vl]; i < win.ptr[vl + 1]; ++i) {
+        const int x = win.idx[i];
+        const int mx = b.st_model[x];
+        if (!no_same && mx != -1) {
+            if (out) {
+                const double bonus = w.lambda_s * b.model_switch[mx] * w.switch_x * w.state_scale;
+                const bool same = mx == mv;
+                out[n] = V6Op{same ? bonus : -bonus, -1, same ? V6_KEY_ALWAYS : V6_KEY_MODEL + mx};
+            }
+            ++n;
+        }
+        const int gx = b.st_group[x];
+        if (!no_pre && gx != -1 && gx == gv) {
+            if (out) {
+                const int Px = b.st_prompt[x];
+                const int shared = Pv < Px ? Pv : Px;
+                out[n] = V6Op{w.lambda_p * w.kappa_prefix * (double)shared / 1000.0 * w.prefix_x *
+                                  w.prefix_scale,
+                              -1, V6_KEY_ALWAYS};
+            }
+            ++n;
+        }
+        if (!no_loc) {
+            for (int e = b.par_ptr[x]; e < b.par_ptr[x + 1]; ++e) {
+                const int pp = b.par_idx[e];
+                if (pp == v) continue;
+                if (out)
+                    out[n] = V6Op{b.has_overrides ? der.edge_sigma[e] : -der.edge_term[e], pp, 0};
+                ++n;
+            }
+        }
+    }
+    return n;
+}
+
+__global__ void fate_template_count_kernel(fate_bank b, fate_weights w, fate_windows win,
+                                           fate_derived der, long long* counts) {
+    const long long vl = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (vl >= (long long)b.n_stages * win.levels) return;
+    counts[vl] = v6_template_walk(b, w, win, der, vl, nullptr);
+}
+
+__global__ void fate_template_fill_kernel(fate_bank b, fate_weights w, fate_windows win,
+                                          fate_derived der) {
+    const long long vl = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (vl >= (long long)b.n_stages * win.levels) return;
+    v6_template_walk(b, w, win, der, vl,
+                     reinterpret_cast<V6Op*>(der.tmpl) + der.tmpl_ptr[vl]);
+}
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+
+// aff_j += val for every device slot j that the op applies to:
+//   key <  1000: applies unless key == device (key 999 = every device)
+//   key >= 1000: applies iff key == tgt_j (= 1000 + displaced resident model)
+template <int DPL>
+__device__ __forceinline__ void v6_apply(double (&aff)[DPL], double val, int k, const int (&d)[DPL],
+                                         const int (&tgt)[DPL]) {
+    if (DPL == 1) {
+        asm("{\n\t.reg .pred q, p;\n\t"
+            "setp.lt.s32 q, %2, 1000;\n\t"
+            "setp.ne.and.s32 p, %2, %3, q;\n\t"
+            "setp.eq.or.s32 p, %2, %4, p;\n\t"
+            "@p add.rn.f64 %0, %0, %1;\n\t}"
+            : "+d"(aff[0])
+            : "d"(val), "r"(k), "r"(d[0]), "r"(tgt[0]));
+    } else {
+        asm("{\n\t.reg .pred q, p, r;\n\t"
+            "setp.lt.s32 q, %3, 1000;\n\t"
+            "setp.ne.and.s32 p, %3, %4, q;\n\t"
+            "setp.eq.or.s32 p, %3, %6, p;\n\t"
+            "setp.ne.and.s32 r, %3, %5, q;\n\t"
+            "setp.eq.or.s32 r, %3, %7, r;\n\t"
+            "@p add.rn.f64 %0, %0, %2;\n\t"
+            "@r add.rn.f64 %1, %1, %2;\n\t}"
+            : "+d"(aff[0]), "+d"(aff[DPL - 1])
+            : "d"(val), "r"(k), "r"(d[0]), "r"(d[DPL - 1]), "r"(tgt[0]), "r"(tgt[DPL - 1]));
+    }
+}
+
+struct V6Item {
+    int q0, nq, m, Pv;
+    long long dev_row0;
+    int cap4;
+    double pcoef, pscale, decode, cplx;
+};
+
+// cache-aware query_compute of query q on device dv (costs.py:70-94) with the
+// device's effective stage part sp
+__device__ __forceinline__ double v6_qc(const fate_bank& b, const fate_state& st,
+                                        const V6Item& it, const int* key, int dv, int q) {
+    const long long sp = key[dv];
+    long long qp = b.q_prompt[it.q0 + q];
+    const int qg = b.q_group[it.q0 + q];
+    if (qg != -1) {
+        const long long drow = it.dev_row0 + dv;
+        const long long cc = cached_tokens(st.kappa + drow * it.cap4, st.kappa_n[drow], qg, it.m);
+        qp = qp - cc > 0 ? qp - cc : 0;
+    }
+    return qc_value(sp, qp, it.pcoef, it.pscale, it.decode, it.cplx, b.dev_speed[dv]);
+}
+
+// ---------------------------------------------------------------------------
+// scoring kernel
+// ---------------------------------------------------------------------------
+
+template <int DPL, bool OVR, int MINB>
+__global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, fate_weights w,
+                                                                  fate_windows win,
+                                                                  fate_derived der, fate_state st,
+                                                                  fate_work work, fate_out out,
+                                                                  V6Layout lay) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int wi = threadIdx.x >> 5, t = threadIdx.x & 31;
+    const long long item = (long long)blockIdx.x * 4 + wi;
+    if (item >= work.n_items) return;  // whole warps exit together
+    unsigned char* sb = smem_raw + lay.item_bytes * wi;
+    double* const s_rows = reinterpret_cast<double*>(sb + lay.rows);
+    double* const s_shard = reinterpret_cast<double*>(sb + lay.shard);
+    double* const s_aware = reinterpret_cast<double*>(sb + lay.aware);
+    double* const s_sw = reinterpret_cast<double*>(sb + lay.sw);
+    double* const s_tr = reinterpret_cast<double*>(sb + lay.tr);
+    double* const s_opval = reinterpret_cast<double*>(sb + lay.opval);
+    int* const s_opkey = reinterpret_cast<int*>(sb + lay.opkey);
+    int* const s_key = reinterpret_cast<int*>(sb + lay.key);
+    int* const s_cslot = reinterpret_cast<int*>(sb + lay.cslot);
+    int* const s_rowdev = reinterpret_cast<int*>(sb + lay.rowdev);
+
+    const unsigned FULL = 0xffffffffu;
+    const int D = b.n_devices, Bmax = b.max_queries, LV = win.levels;
+    const bool no_loc = w.ablation & FATE_NO_LOCALITY;
+    const bool no_shard = w.ablation & FATE_NO_SHARD;
+    const int H = w.eff_horizon;
+    const int M1 = b.n_models + 1;
+
+    // ---- item header: work entry, stage record, scenario scalars ----------------------------
+    const int s = work.scen[item];
+    const int v = work.stage[item];
+    const V6Stage* srec = reinterpret_cast<const V6Stage*>(der.stage_rec) + v;
+    const int4 h0 = __ldg(reinterpret_cast<const int4*>(srec) + 0);
+    const int4 h1 = __ldg(reinterpret_cast<const int4*>(srec) + 1);
+    const int4 h2 = __ldg(reinterpret_cast<const int4*>(srec) + 2);
+    const longlong2 h3 = __ldg(reinterpret_cast<const longlong2*>(srec) + 3);
+    const double2 c0 = __ldg(reinterpret_cast<const double2*>(srec) + 4);
+    const double2 c1 = __ldg(reinterpret_cast<const double2*>(srec) + 5);
+    const double2 c2 = __ldg(reinterpret_cast<const double2*>(srec) + 6);
+    const double clock = st.scen_clock[s];
+    const long long loc_off = st.scen_loc_off[s];
+    const int done_lvl = st.scen_done_level[s];
+
+    V6Item it;
+    it.m = h0.x;
+    const int m = it.m, R = h0.y, gv = h0.z;
+    it.Pv = h0.w;
+    const int pa0 = h1.x, pa1 = h1.y;
+    it.q0 = h1.z;
+    it.nq = h1.w;
+    const int nq = it.nq;
+    const int32_t* loc_row = st.loc + loc_off - h2.x;
+    const int sflags = h2.y;
+    const int bound = h2.z;
+    const uint64_t elig = (uint64_t)h3.x;
+    const bool cache_reuse = sflags & V6_CACHE_REUSE;
+    const bool per_device_rows = sflags & V6_QGROUPS;
+    it.pcoef = c0.x;
+    it.pscale = c0.y;
+    it.decode = c1.x;
+    it.cplx = c1.y;
+    const double swv = c2.x;
+    it.dev_row0 = (long long)s * D;
+    it.cap4 = st.kappa_cap * 4;
+
+    // ---- device rows that everything below needs ----------------------------------------------
+    int res0[DPL], dv[DPL];
+    bool live[DPL];
+    double fr[DPL];
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+        dv[j] = t + 32 * j;
+        live[j] = dv[j] < D;
+        res0[j] = live[j] ? st.residency[it.dev_row0 + dv[j]] : -1;
+        fr[j] = live[j] ? st.dev_free[it.dev_row0 + dv[j]] : 0.0;
+    }
+
+    // ---- prefetch: located-parent flag per horizon level and the static full tail --------
+    const bool do_tail = H > 1;
+    unsigned walk_m = 0u;  // bit l: level l has a locality op (needs the op-list walk)
+    double tail_full[DPL];
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) tail_full[j] = 0.0;
+    if (do_tail) {
+        const double* row = der.tail_sum + (size_t)v * M1;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) {
+            const int r = res0[j];
+            tail_full[j] = row[(r != -1 && r != m && r < b.n_models) ? 1 + r : 0];
+        }
+        if (!no_loc) {
+            // a window parent above the scenario's highest located stage cannot be
+            // located: levels whose parents all lie above it need no gather
+            for (int l = 0; l < LV; ++l) {
+                const long long vl = (long long)v * LV + l;
+                if (win.wpar_minlvl[vl] > done_lvl) continue;
+                const long long w1 = win.wpar_ptr[vl + 1];
+                bool located = false;
+                for (long long i = win.wpar_ptr[vl] + t; i < w1; i += 32)
+                    located |= loc_row[win.wpar_idx[i]] >= 0;
+                if (__any_sync(FULL, located)) walk_m |= 1u << (l < 31 ? l : 31);
+            }
+        }
+    }
+    const double rsum = t < 6 ? der.row_sums[(size_t)v * 6 + t] : 0.0;  // static-class sums
+
+    // ---- P0: per-device stage part, switch; v's parents --------------------------------------
+    int cs[DPL], hit[DPL];
+    bool ok[DPL];
+    double trv[DPL];
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+        ok[j] = live[j] && ((elig >> dv[j]) & 1ull);
+        cs[j] = it.Pv;
+        hit[j] = 0;
+        trv[j] = 0.0;
+        if (live[j]) {
+            if (cache_reuse) {
+                const long long row = it.dev_row0 + dv[j];
+                const int c = cached_tokens(st.kappa + row * it.cap4, st.kappa_n[row], gv, m);
+                cs[j] = it.Pv - c > 0 ? it.Pv - c : 0;
+            }
+            s_key[dv[j]] = cs[j];
+            s_sw[dv[j]] = res0[j] == m ? 0.0 : swv;
+        }
+    }
+    // v's parents: lane-parallel fetch, broadcast in ascending order
+    // (transfer_cost, costs.py:113-125; colo counts, costs.py:160-165)
+    for (int e0 = pa0; e0 < pa1; e0 += 32) {
+        const int e = e0 + t;
+        int L = -1;
+        double sg = 0.0;
+        if (e < pa1) {
+            L = loc_row[b.par_idx[e]];
+            sg = der.edge_sigma[e];
+        }
+        const int n = pa1 - e0 < 32 ? pa1 - e0 : 32;
+        for (int i = 0; i < n; ++i) {
+            const int Li = __shfl_sync(FULL, L, i);
+            const double si = __shfl_sync(FULL, sg, i);
+            if (Li < 0) continue;
+#pragma unroll
+            for (int j = 0; j < DPL; ++j) {
+                hit[j] += Li == dv[j];
+                if (live[j] && Li != dv[j]) {
+                    const double beta = OVR ? b.beta[(size_t)Li * D + dv[j]] : b.beta_default;
+                    trv[j] += beta * si;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < DPL; ++j)
+        if (live[j]) s_tr[dv[j]] = trv[j] * w.transfer_x;
+    unsigned long long idle_m = 0ull, ok_m = 0ull;
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+        idle_m |= (unsigned long long)__ballot_sync(FULL, ok[j] && fr[j] <= clock + 1e-12) << (32 * j);
+        ok_m |= (unsigned long long)__ballot_sync(FULL, ok[j]) << (32 * j);
+    }
+    __syncwarp();
+
+    // ---- P1: row classes ------------------------------------------------------------------------
+    const bool uniform = b.flags & FATE_BANK_UNIFORM_SPEED;
+    int rep[DPL];
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+        unsigned same = (unsigned)(ok_m >> (32 * j));
+        if (!per_device_rows) {
+            same &= __match_any_sync(FULL, cs[j]);
+            if (!uniform) {
+                const unsigned long long spd =
+                    __double_as_longlong(b.dev_speed[live[j] ? dv[j] : 0]);
+                same &= __match_any_sync(FULL, spd);
+            }
+        } else {
+            same &= 1u << t;
+        }
+        rep[j] = ok[j] ? 32 * j + __ffs(same) - 1 : -1;
+    }
+    if (DPL == 2 && !per_device_rows) {
+        // a slot-1 class may already exist among slot-0 devices
+        const unsigned reps0 = __ballot_sync(FULL, ok[0] && rep[0] == dv[0]);
+        if (ok[DPL - 1]) {
+            unsigned rr = reps0;
+            const double sp = b.dev_speed[dv[DPL - 1]];
+            while (rr) {
+                const int e = __ffs(rr) - 1;
+                rr &= rr - 1;
+                if (s_key[e] == cs[DPL - 1] && (uniform || b.dev_speed[e] == sp)) {
+                    rep[DPL - 1] = e;
+                    break;
+                }
+            }
+        }
+    }
+    unsigned long long rep_m = 0ull;
+#pragma unroll
+    for (int j = 0; j < DPL; ++j)
+        rep_m |= (unsigned long long)__ballot_sync(FULL, ok[j] && rep[j] == dv[j]) << (32 * j);
+    const int n_idle = __popcll(idle_m);
+    int kb = 0, ki = 0;
+    if (R > 1 && !no_shard) {
+        kb = R < 1 + n_idle ? R : 1 + n_idle;
+        ki = R < n_idle ? R : n_idle;
+    }
+    const bool kb_ok = kb >= 2 && kb <= V6_KT;
+    const bool ki_ok = ki != kb && ki >= 2 && ki <= V6_KT;
+    const int per = 1 + (kb_ok ? kb : 0) + (ki_ok ? ki : 0);
+    // static classes: representatives with sp == P (A) and sp == 0 < P (B)
+    unsigned long long am = 0ull, bm = 0ull;
+    if (uniform && !per_device_rows && kb <= 2 && ki <= 2) {
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) {
+            const bool r0 = ok[j] && rep[j] == dv[j];
+            am |= (unsigned long long)__ballot_sync(FULL, r0 && cs[j] == it.Pv) << (32 * j);
+            bm |= (unsigned long long)__ballot_sync(FULL, r0 && cs[j] == 0 && it.Pv > 0) << (32 * j);
+        }
+    }
+    const unsigned long long dyn_m = rep_m & ~am & ~bm;  // representatives of dynamic classes
+    const int n_dyn = __popcll(dyn_m);
+    const int n_rows = n_dyn < V6_RCAP ? n_dyn : V6_RCAP;
+    // table slot of each device's class: 0 = A, 1 = B, 2 + row slot, -1 = direct
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+        if (!ok[j]) continue;
+        const unsigned long long rb = 1ull << rep[j];
+        int slot;
+        if (am & rb) slot = 0;
+        else if (bm & rb) slot = 1;
+        else {
+            const int r = __popcll(dyn_m & low_mask(rep[j]));
+            slot = r < V6_RCAP ? 2 + r : -1;
+            if (rep[j] == dv[j] && r < V6_RCAP) s_rowdev[r] = dv[j];
+        }
+        s_cslot[dv[j]] = slot;
+    }
+    if (t < 6) {
+        // lane t holds row_sums[v][t]: class si = t / 3, entry e = t % 3 (full, shard 0, 1)
+        const int si = t / 3, e = t - 3 * si;
+        if (si == 0 ? am != 0ull : bm != 0ull) {
+            if (e == 0) {
+                s_aware[si] = rsum;
+            } else {
+                if (kb == 2) s_shard[(si * 2 + 0) * V6_KT + (e - 1)] = rsum;
+                if (ki == 2 && ki != kb) s_shard[(si * 2 + 1) * V6_KT + (e - 1)] = rsum;
+            }
+        }
+    }
+    __syncwarp();
+
+    // ---- P2: dynamic class rows and sums -------------------------------------------------
+    for (int p = t; p < n_rows * nq; p += 32) {
+        const int r = p / nq, q = p - r * nq;
+        s_rows[r * Bmax + q] = v6_qc(b, st, it, s_key, s_rowdev[r], q);
+    }
+    __syncwarp();
+    for (int p = t; p < n_rows * per; p += 32) {
+        const int r = p / per;
+        int j = p - r * per;
+        const double* row = s_rows + r * Bmax;
+        const int slot = 2 + r;
+        PySum acc;
+        if (j == 0) {
+            for (int q = 0; q < nq; ++q) acc.add(row[q]);
+            s_aware[slot] = acc.result();
+        } else {
+            j -= 1;
+            int kslot = 0, k = kb;
+            if (!kb_ok || j >= kb) {
+                if (kb_ok) j -= kb;
+                kslot = 1;
+                k = ki;
+            }
+            int lo, hi;
+            shard_range(nq, k, j, &lo, &hi);
+            for (int q = lo; q < hi; ++q) acc.add(row[q]);
+            s_shard[(slot * 2 + kslot) * V6_KT + j] = acc.result();
+        }
+    }
+    __syncwarp();
+
+    // aware per device and base_best (costs.py:257-259); classes without a slot
+    // (more than RCAP dynamic classes) are summed directly by their lanes
+    double here[DPL];
+    double bb = 0.0;
+    {
+        bool have = false;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) {
+            here[j] = 0.0;
+            if (!ok[j]) continue;
+            const int slot = s_cslot[dv[j]];
+            if (slot >= 0) {
+                here[j] = s_aware[slot];
+            } else {
+                PySum acc;
+                for (int q = 0; q < nq; ++q) acc.add(v6_qc(b, st, it, s_key, dv[j], q));
+                here[j] = acc.result();
+            }
+            if (!have || here[j] < bb) bb = here[j];
+            have = true;
+        }
+        // warp min over lanes with a value (min is order-free)
+        double cand = have ? bb : __longlong_as_double(0x7ff0000000000000LL);  // +inf
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(FULL, cand, o);
+            cand = y < cand ? y : cand;
+        }
+        bb = cand;
+    }
+
+    // ---- P3: tail ---------------------------------------------------------------------------------
+    double tail[DPL];
+    int dmc[DPL], tgt[DPL];
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+        tail[j] = 0.0;
+        dmc[j] = (live[j] && res0[j] != -1 && res0[j] != m && res0[j] < b.n_models) ? res0[j] : -1;
+        tgt[j] = dmc[j] >= 0 ? V6_KEY_MODEL + dmc[j] : -2;
+    }
+    if (do_tail && walk_m == 0u) {
+        // no locality op anywhere in the horizon: the whole tail is static
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) tail[j] = tail_full[j];
+    } else if (do_tail) {
+        const V6Op* tmpl = reinterpret_cast<const V6Op*>(der.tmpl);
+        for (int l = 0; l < LV; ++l) {
+            const long long vl = (long long)v * LV + l;
+            const long long lo = win.ptr[vl];
+            const int n_b = (int)(win.ptr[vl + 1] - lo);
+            if (n_b == 0) continue;
+            const double dml = der.demand[vl];
+            double aff[DPL];
+            const bool wl = (walk_m >> (l < 31 ? l : 31)) & 1u;
+            if (!wl) {
+                const double* row = der.tail_static + vl * M1;
+#pragma unroll
+                for (int j = 0; j < DPL; ++j) aff[j] = row[1 + dmc[j]];
+            } else {
+                // op list from the level's template: static entries always, edge
+                // entries iff their parent is located (order preserved)
+                const long long t0 = der.tmpl_ptr[vl], t1 = der.tmpl_ptr[vl + 1];
+                int base = 0;
+                for (long long j0 = t0; j0 < t1; j0 += 32) {
+                    const long long jx = j0 + t;
+                    bool keep = false;
+                    double val = 0.0;
+                    int key = 0;
+                    if (jx < t1) {
+                        const int4 raw = __ldg(reinterpret_cast<const int4*>(tmpl + jx));
+                        val = __hiloint2double(raw.y, raw.x);
+                        if (raw.z < 0) {
+                            keep = true;
+                            key = raw.w;
+                        } else {
+                            const int L = loc_row[raw.z];
+                            keep = L >= 0;
+                            key = OVR ? V6_KEY_SIGMA + L : L;
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(FULL, keep);
+                    if (keep) {
+                        const int pos = base + __popc(bal & ((1u << t) - 1u));
+                        s_opval[pos] = val;
+                        s_opkey[pos] = key;
+                    }
+                    base += __popc(bal);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < DPL; ++j) aff[j] = 0.0;
+                if (!OVR) {
+#pragma unroll 4
+                    for (int o = 0; o < base; ++o) v6_apply<DPL>(aff, s_opval[o], s_opkey[o], dv, tgt);
+                } else {
+                    for (int o = 0; o < base; ++o) {
+                        const int k = s_opkey[o];
+                        const double val = s_opval[o];
+#pragma unroll
+                        for (int j = 0; j < DPL; ++j) {
+                            if (k < V6_KEY_MODEL) {
+                                if (k != dv[j]) aff[j] += val;
+                            } else if (k < V6_KEY_SIGMA) {
+                                if (k - V6_KEY_MODEL == dmc[j]) aff[j] += val;
+                            } else if (k - V6_KEY_SIGMA != dv[j]) {
+                                aff[j] -= w.lambda_tr *
+                                          b.beta[(size_t)(k - V6_KEY_SIGMA) * D +
+                                                 (live[j] ? dv[j] : 0)] *
+                                          val * w.transfer_x * w.locality_scale;
+                            }
+                        }
+                    }
+                }
+                __syncwarp();  // op buffer reused by the next level
+            }
+#pragma unroll
+            for (int j = 0; j < DPL; ++j)
+                tail[j] += w.gamma_pow[l + 1] * (aff[j] / (double)n_b + w.demand_coeff * dml);
+        }
+    }
+
+    // ---- P4: per-device assembly ----------------------------------------------------------------
+    double* psi = out.psi + work.psi_off[item];
+    const double split = no_loc ? 0.0 : (bound > 1 ? c2.y : 0.0);
+    const bool no_pre = w.ablation & FATE_NO_PREFIX;
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+        if (!live[j]) continue;
+        const int d = dv[j];
+        const long long orow = item * D + d;
+        if (!ok[j]) {
+            const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+            for (int k = 0; k < bound; ++k) psi[(long long)k * D + d] = qnan;
+            if (out.sched) out.sched[orow] = qnan;
+            if (out.tail) out.tail[orow] = qnan;
+            if (out.completion) out.completion[orow] = qnan;
+            continue;
+        }
+        const double wait = py_max0(fr[j] - clock);
+        const double sw = s_sw[d];
+        const double tr = s_tr[d];
+        // 0 / n == +0.0 exactly: divide only when a parent is co-located
+        const double colo = (pa1 > pa0 && hit[j] > 0) ? (double)hit[j] / (double)(pa1 - pa0) : 0.0;
+
+        // prefix_overlap_thousands (costs.py:127-145), integer-exact
+        long long tokens = 0;
+        if (cache_reuse) tokens += it.Pv - cs[j];  // min(cached, P) = P - sp
+        if (per_device_rows) {
+            const long long row = it.dev_row0 + d;
+            const int32_t* kap = st.kappa + row * it.cap4;
+            const int kn = st.kappa_n[row];
+            for (int q = 0; q < nq; ++q) {
+                const int qg = b.q_group[it.q0 + q];
+                if (qg == -1) continue;
+                const long long c = cached_tokens(kap, kn, qg, m);
+                const long long qp = b.q_prompt[it.q0 + q];
+                tokens += c < qp ? c : qp;
+            }
+        }
+        const double prefix =
+            w.kappa_prefix * (tokens == 0 ? 0.0 : (double)tokens / 1000.0) * w.prefix_x;
+
+        // _parallel_benefit (costs.py:181-201)
+        const double full_total = sw + tr + here[j];
+        double parallel = 0.0;
+        if (R > 1 && !no_shard) {
+            const bool self_idle = (idle_m >> d) & 1ull;
+            const int others = n_idle - (self_idle ? 1 : 0);
+            const int k = R < 1 + others ? R : 1 + others;
+            if (k > 1) {
+                const int kslot = (k == kb && kb_ok) ? 0 : 1;
+                const bool tab = kslot == 0 || (k == ki && ki_ok);
+                unsigned long long rest = idle_m & ~(1ull << d);
+                double worst = 0.0;
+                for (int i = 0; i < k; ++i) {
+                    int dev = d;
+                    if (i > 0) {
+                        dev = __ffsll((long long)rest) - 1;
+                        rest &= rest - 1;
+                    }
+                    const int slot = s_cslot[dev];
+                    double ssum;
+                    if (tab && slot >= 0) {
+                        ssum = s_shard[(slot * 2 + kslot) * V6_KT + i];
+                    } else {
+                        int lo, hi;
+                        shard_range(nq, k, i, &lo, &hi);
+                        PySum acc;
+                        for (int q = lo; q < hi; ++q)
+                            acc.add(slot >= 2 ? s_rows[(slot - 2) * Bmax + q]
+                                              : v6_qc(b, st, it, s_key, dev, q));
+                        ssum = acc.result();
+                    }
+                    const double tot = s_sw[dev] + s_tr[dev] + ssum;
+                    if (i == 0 || tot > worst) worst = tot;
+                }
+                const double overhead = w.shard_overhead_frac * here[j] * (double)(k - 1);
+                parallel = py_max0(full_total - worst - overhead);
+            }
+        }
+
+        // sched_score (costs.py:210-231)
+        const double tr_s = no_loc ? 0.0 : tr;
+        const double colo_s = no_loc ? 0.0 : colo;
+        const double prefix_s = no_pre ? 0.0 : prefix;
+        const double par_s = no_shard ? 0.0 : parallel;
+        const double S = -w.lambda_q * wait - w.lambda_s * sw * w.state_scale
+                         - w.lambda_tr * tr_s * w.locality_scale
+                         + w.lambda_c * colo_s * w.locality_scale
+                         + w.lambda_p * prefix_s * w.prefix_scale + w.lambda_r * par_s;
+
+        if (out.sched) out.sched[orow] = S;
+        if (out.tail) out.tail[orow] = tail[j];
+        if (out.completion) out.completion[orow] = wait + full_total;
+        psi[d] = S + tail[j];
+
+        // _marginal_shard_score (costs.py:249-279)
+        if (bound > 1) {
+            const double hv = here[j] > bb ? here[j] : bb;
+            const double overhead = w.shard_overhead_frac * bb;
+            const double tr_m = no_loc ? 0.0 : tr;
+            for (int k = 1; k < bound; ++k) {
+                // x / 1 == x and x / 2 == x * 0.5 exactly (both correctly rounded x/2)
+                const double q1 = k == 1 ? bb : bb / (double)k;
+                const double q2 = k == 1 ? hv * 0.5 : hv / (double)(k + 1);
+                const double reduction = q1 - q2;
+                psi[(long long)k * D + d] = w.lambda_r * (reduction - overhead) -
+                                            w.lambda_q * wait - w.lambda_s * sw * w.state_scale -
+                                            w.lambda_tr * (tr_m + split) * w.locality_scale;
+            }
+        }
+    }
+}

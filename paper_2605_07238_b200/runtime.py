@@ -54,6 +54,8 @@ def load_library():
     L.fate_window_parents_host.restype = C.c_int
     L.fate_window_parents_host.argtypes = [C.c_int32, C.c_int32] + [C.c_void_p] * 6 + [
         C.POINTER(C.c_int64)]
+    L.fate_template_count.restype = C.c_int
+    L.fate_template_count.argtypes = [C.c_void_p] * 6
     L.fate_prepare.restype = C.c_int
     L.fate_prepare.argtypes = [C.c_void_p] * 5
     L.fate_score.restype = C.c_int
@@ -70,7 +72,7 @@ def load_library():
     L.fate_pipeline_replay.argtypes = [C.c_void_p, C.c_void_p]
     L.fate_pipeline_bytes.restype = C.c_int
     L.fate_pipeline_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
-    if L.fate_abi_version() != 1:
+    if L.fate_abi_version() != 2:
         raise FateUnavailable("libfate.so ABI version mismatch")
     _lib = L
     return L
@@ -249,6 +251,7 @@ class DeviceBank:
         self.tail_sum = torch.empty(max(n * (packed.scalars["n_models"] + 1), 1), **f64)
         n_static = n * self.levels * (packed.scalars["n_models"] + 1)
         self.tail_static = torch.empty(max(n_static, 1), **f64)
+        self.stage_rec = torch.empty(max(n, 1) * 112, dtype=torch.uint8, device=self.device)
         self.cder = abi.FateDerived(mean_base=self.mean_base.data_ptr(),
                                     demand=self.demand.data_ptr(),
                                     split_penalty=self.split_penalty.data_ptr(),
@@ -257,8 +260,24 @@ class DeviceBank:
                                     row_sums=self.row_sums.data_ptr(),
                                     inst_qgroups=self.inst_qgroups.data_ptr(),
                                     tail_sum=self.tail_sum.data_ptr(),
-                                    tail_static=self.tail_static.data_ptr())
+                                    tail_static=self.tail_static.data_ptr(),
+                                    stage_rec=self.stage_rec.data_ptr())
         s = stream or torch.cuda.current_stream(self.device)
+        # op templates of the tail (v6 kernel): count per (stage, level), scan, fill
+        nvl = n * self.levels
+        self.tmpl_ptr = torch.zeros(nvl + 1, dtype=torch.int64, device=self.device)
+        if nvl:
+            counts = torch.empty(nvl, dtype=torch.int64, device=self.device)
+            _check(L.fate_template_count(C.byref(self.cbank), C.byref(self.cweights),
+                                         C.byref(self.cwin), C.byref(self.cder),
+                                         C.c_void_p(counts.data_ptr()), C.c_void_p(s.cuda_stream)),
+                   "fate_template_count")
+            with torch.cuda.stream(s):
+                torch.cumsum(counts, 0, out=self.tmpl_ptr[1:])
+        n_tmpl = int(self.tmpl_ptr[-1].item()) if nvl else 0
+        self.tmpl = torch.empty(max(n_tmpl, 1) * 16, dtype=torch.uint8, device=self.device)
+        self.cder.tmpl_ptr = self.tmpl_ptr.data_ptr()
+        self.cder.tmpl = self.tmpl.data_ptr()
         _check(L.fate_prepare(C.byref(self.cbank), C.byref(self.cweights), C.byref(self.cwin),
                               C.byref(self.cder), C.c_void_p(s.cuda_stream)), "fate_prepare")
 

@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     assert {"fate_score", "fate_prepare", "fate_windows_build_host"} <= set(names)
     for n in names:
         assert hasattr(lib, n), n
-    assert runtime.load_library().fate_abi_version() == 1
+    assert runtime.load_library().fate_abi_version() == 2
 
 
 def _py_windows(bank, levels):
