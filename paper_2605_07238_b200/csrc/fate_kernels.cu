@@ -544,9 +544,14 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(fate_score_v6_kernel<DPL, OVR, MINB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const unsigned blocks = (unsigned)((work->n_items + 3) / 4);
+    static int ipc = -1;
+    if (ipc < 0) {
+        const char* e = getenv("FATE_V6_IPC");
+        ipc = e ? std::max(1, atoi(e)) : V6_IPC;
+    }
+    const unsigned blocks = (unsigned)((work->n_items + ipc - 1) / ipc);
     fate_score_v6_kernel<DPL, OVR, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
-                                                                    *work, *out, lay);
+                                                                    *work, *out, lay, ipc);
     return 0;
 }
 

@@ -35,6 +35,7 @@ constexpr int V6_SLOTS = V6_RCAP + 2;  // table slots: 0 = static A, 1 = static 
 constexpr int V6_KEY_ALWAYS = 999;     // op applied on every device (same-model, prefix)
 constexpr int V6_KEY_MODEL = 1000;     // op key >= this: displacement op of model key-1000
 constexpr int V6_KEY_SIGMA = 2000;     // OVR edge op: key-2000 = location, val = sigma
+constexpr int V6_KEY_NOOP = 0x7ffffff0;  // padding op: matches no device (val +0.0)
 
 // stage record flags
 constexpr int V6_CACHE_REUSE = 1;  // cache_reuse and a stage group
@@ -79,8 +80,9 @@ inline V6Layout v6_layout(int D, int Bmax, int ops_cap) {
     L.aware = take(V6_SLOTS, 8);
     L.sw = take(D, 8);
     L.tr = take(D, 8);
-    L.opval = take(ops_cap > 0 ? ops_cap : 1, 8);
-    L.opkey = take(ops_cap > 0 ? ops_cap : 1, 4);
+    const int ops4 = ((ops_cap > 0 ? ops_cap : 1) + 3) & ~3;  // walked 4 at a time
+    L.opval = take(ops4, 8);
+    L.opkey = take(ops4, 4);
     L.key = take(D, 4);
     L.cslot = take(D, 4);
     L.rowdev = take(V6_RCAP, 4);
@@ -247,17 +249,14 @@ __device__ __forceinline__ double v6_qc(const fate_bank& b, const fate_state& st
 // scoring kernel
 // ---------------------------------------------------------------------------
 
-template <int DPL, bool OVR, int MINB>
-__global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, fate_weights w,
-                                                                  fate_windows win,
-                                                                  fate_derived der, fate_state st,
-                                                                  fate_work work, fate_out out,
-                                                                  V6Layout lay) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int wi = threadIdx.x >> 5, t = threadIdx.x & 31;
-    const long long item = (long long)blockIdx.x * 4 + wi;
-    if (item >= work.n_items) return;  // whole warps exit together
-    unsigned char* sb = smem_raw + lay.item_bytes * wi;
+// One item (scenario, stage v) by one warp; sb = the warp's shared-memory slice.
+template <int DPL, bool OVR>
+__device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& w,
+                                        const fate_windows& win, const fate_derived& der,
+                                        const fate_state& st, const fate_work& work,
+                                        const fate_out& out, const V6Layout& lay,
+                                        const long long item, unsigned char* sb) {
+    const int t = threadIdx.x & 31;
     double* const s_rows = reinterpret_cast<double*>(sb + lay.rows);
     double* const s_shard = reinterpret_cast<double*>(sb + lay.shard);
     double* const s_aware = reinterpret_cast<double*>(sb + lay.aware);
@@ -341,11 +340,13 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
         if (!no_loc) {
             // a window parent above the scenario's highest located stage cannot be
             // located: levels whose parents all lie above it need no gather
+            #pragma unroll 1
             for (int l = 0; l < LV; ++l) {
                 const long long vl = (long long)v * LV + l;
                 if (win.wpar_minlvl[vl] > done_lvl) continue;
                 const long long w1 = win.wpar_ptr[vl + 1];
                 bool located = false;
+                #pragma unroll 1
                 for (long long i = win.wpar_ptr[vl] + t; i < w1; i += 32)
                     located |= loc_row[win.wpar_idx[i]] >= 0;
                 if (__any_sync(FULL, located)) walk_m |= 1u << (l < 31 ? l : 31);
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
     }
     // v's parents: lane-parallel fetch, broadcast in ascending order
     // (transfer_cost, costs.py:113-125; colo counts, costs.py:160-165)
+    #pragma unroll 1
     for (int e0 = pa0; e0 < pa1; e0 += 32) {
         const int e = e0 + t;
         int L = -1;
@@ -385,6 +387,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
             sg = der.edge_sigma[e];
         }
         const int n = pa1 - e0 < 32 ? pa1 - e0 : 32;
+        #pragma unroll 1
         for (int i = 0; i < n; ++i) {
             const int Li = __shfl_sync(FULL, L, i);
             const double si = __shfl_sync(FULL, sg, i);
@@ -500,11 +503,13 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
     __syncwarp();
 
     // ---- P2: dynamic class rows and sums -------------------------------------------------
+    #pragma unroll 1
     for (int p = t; p < n_rows * nq; p += 32) {
         const int r = p / nq, q = p - r * nq;
         s_rows[r * Bmax + q] = v6_qc(b, st, it, s_key, s_rowdev[r], q);
     }
     __syncwarp();
+    #pragma unroll 1
     for (int p = t; p < n_rows * per; p += 32) {
         const int r = p / per;
         int j = p - r * per;
@@ -512,6 +517,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
         const int slot = 2 + r;
         PySum acc;
         if (j == 0) {
+            #pragma unroll 1
             for (int q = 0; q < nq; ++q) acc.add(row[q]);
             s_aware[slot] = acc.result();
         } else {
@@ -524,6 +530,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
             }
             int lo, hi;
             shard_range(nq, k, j, &lo, &hi);
+            #pragma unroll 1
             for (int q = lo; q < hi; ++q) acc.add(row[q]);
             s_shard[(slot * 2 + kslot) * V6_KT + j] = acc.result();
         }
@@ -545,6 +552,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
                 here[j] = s_aware[slot];
             } else {
                 PySum acc;
+                #pragma unroll 1
                 for (int q = 0; q < nq; ++q) acc.add(v6_qc(b, st, it, s_key, dv[j], q));
                 here[j] = acc.result();
             }
@@ -576,6 +584,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
         for (int j = 0; j < DPL; ++j) tail[j] = tail_full[j];
     } else if (do_tail) {
         const V6Op* tmpl = reinterpret_cast<const V6Op*>(der.tmpl);
+        #pragma unroll 1
         for (int l = 0; l < LV; ++l) {
             const long long vl = (long long)v * LV + l;
             const long long lo = win.ptr[vl];
@@ -593,6 +602,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
                 // entries iff their parent is located (order preserved)
                 const long long t0 = der.tmpl_ptr[vl], t1 = der.tmpl_ptr[vl + 1];
                 int base = 0;
+                #pragma unroll 1
                 for (long long j0 = t0; j0 < t1; j0 += 32) {
                     const long long jx = j0 + t;
                     bool keep = false;
@@ -618,13 +628,30 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
                     }
                     base += __popc(bal);
                 }
-                __syncwarp();
 #pragma unroll
                 for (int j = 0; j < DPL; ++j) aff[j] = 0.0;
                 if (!OVR) {
-#pragma unroll 4
-                    for (int o = 0; o < base; ++o) v6_apply<DPL>(aff, s_opval[o], s_opkey[o], dv, tgt);
+                    // pad to a multiple of 4 with no-op entries; walk 4 ops per
+                    // iteration with one 16-byte key load and two 16-byte value loads
+                    const int nb4 = (base + 3) & ~3;
+                    if (t < nb4 - base) {
+                        s_opval[base + t] = 0.0;
+                        s_opkey[base + t] = V6_KEY_NOOP;
+                    }
+                    __syncwarp();
+                    #pragma unroll 1
+                    for (int o = 0; o < nb4; o += 4) {
+                        const int4 k4 = *reinterpret_cast<const int4*>(s_opkey + o);
+                        const double2 va = *reinterpret_cast<const double2*>(s_opval + o);
+                        const double2 vb = *reinterpret_cast<const double2*>(s_opval + o + 2);
+                        v6_apply<DPL>(aff, va.x, k4.x, dv, tgt);
+                        v6_apply<DPL>(aff, va.y, k4.y, dv, tgt);
+                        v6_apply<DPL>(aff, vb.x, k4.z, dv, tgt);
+                        v6_apply<DPL>(aff, vb.y, k4.w, dv, tgt);
+                    }
                 } else {
+                    __syncwarp();
+                    #pragma unroll 1
                     for (int o = 0; o < base; ++o) {
                         const int k = s_opkey[o];
                         const double val = s_opval[o];
@@ -662,6 +689,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
         const long long orow = item * D + d;
         if (!ok[j]) {
             const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+            #pragma unroll 1
             for (int k = 0; k < bound; ++k) psi[(long long)k * D + d] = qnan;
             if (out.sched) out.sched[orow] = qnan;
             if (out.tail) out.tail[orow] = qnan;
@@ -681,6 +709,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
             const long long row = it.dev_row0 + d;
             const int32_t* kap = st.kappa + row * it.cap4;
             const int kn = st.kappa_n[row];
+            #pragma unroll 1
             for (int q = 0; q < nq; ++q) {
                 const int qg = b.q_group[it.q0 + q];
                 if (qg == -1) continue;
@@ -704,6 +733,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
                 const bool tab = kslot == 0 || (k == ki && ki_ok);
                 unsigned long long rest = idle_m & ~(1ull << d);
                 double worst = 0.0;
+                #pragma unroll 1
                 for (int i = 0; i < k; ++i) {
                     int dev = d;
                     if (i > 0) {
@@ -718,6 +748,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
                         int lo, hi;
                         shard_range(nq, k, i, &lo, &hi);
                         PySum acc;
+                        #pragma unroll 1
                         for (int q = lo; q < hi; ++q)
                             acc.add(slot >= 2 ? s_rows[(slot - 2) * Bmax + q]
                                               : v6_qc(b, st, it, s_key, dev, q));
@@ -751,6 +782,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
             const double hv = here[j] > bb ? here[j] : bb;
             const double overhead = w.shard_overhead_frac * bb;
             const double tr_m = no_loc ? 0.0 : tr;
+            #pragma unroll 1
             for (int k = 1; k < bound; ++k) {
                 // x / 1 == x and x / 2 == x * 0.5 exactly (both correctly rounded x/2)
                 const double q1 = k == 1 ? bb : bb / (double)k;
@@ -761,5 +793,38 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
                                             w.lambda_tr * (tr_m + split) * w.locality_scale;
             }
         }
+    }
+}
+
+// Items are handed to warps from a per-CTA queue of V6_IPC consecutive items
+// (shared-memory ticket counter): a warp that finishes a cheap item takes the
+// next one instead of idling until the slowest warp of its CTA is done, so
+// CTA slots are not held by finished warps (item costs vary several-fold with
+// the number of walked horizon levels).
+constexpr int V6_IPC = 8;  // default items per CTA (FATE_V6_IPC overrides, A/B only)
+
+template <int DPL, bool OVR, int MINB>
+__global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, fate_weights w,
+                                                                  fate_windows win,
+                                                                  fate_derived der, fate_state st,
+                                                                  fate_work work, fate_out out,
+                                                                  V6Layout lay, int ipc) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int s_next;
+    const int wi = threadIdx.x >> 5, t = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+    const long long first = (long long)blockIdx.x * ipc;
+    const long long left = work.n_items - first;
+    const int n = left < ipc ? (int)left : ipc;
+    unsigned char* sb = smem_raw + lay.item_bytes * wi;
+    #pragma unroll 1
+    for (;;) {
+        int i = 0;
+        if (t == 0) i = atomicAdd(&s_next, 1);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= n) break;
+        v6_item<DPL, OVR>(b, w, win, der, st, work, out, lay, first + i, sb);
+        __syncwarp();  // the slice is reused by the next item
     }
 }

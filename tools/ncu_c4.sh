@@ -1,0 +1,3 @@
+#!/bin/bash
+O=$1; mkdir -p $O
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fate_score -s 3 -c 1 -o $O/c4_full python bench.py --workload c4 --mode sweep --steps 3 --warmup 3 --no-cpu > $O/ncu_c4.log 2>&1
