@@ -544,14 +544,28 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(fate_score_v6_kernel<DPL, OVR, MINB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    static int ipc = -1;
-    if (ipc < 0) {
-        const char* e = getenv("FATE_V6_IPC");
-        ipc = e ? std::max(1, atoi(e)) : V6_IPC;
+    // persistent grid: every resident CTA slot once (capped by the item count)
+    static thread_local size_t occ_smem = ~size_t(0);
+    static thread_local int occ_dev = -1, o = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (occ_smem != smem || occ_dev != dev) {
+        int sms = 0, per = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fate_score_v6_kernel<DPL, OVR, MINB>,
+                                                      128, smem);
+        o = std::max(1, sms * std::max(1, per));
+        occ_smem = smem;
+        occ_dev = dev;
     }
-    const unsigned blocks = (unsigned)((work->n_items + ipc - 1) / ipc);
+    if (work->n_items > 0x7fffffffLL - 4 * 128 * V6_FETCH)
+        return fail(FATE_ETOOBIG, "v6: too many items for the 32-bit ticket counter");
+    const long long want = (work->n_items + 3) / 4;
+    const unsigned blocks = (unsigned)std::min<long long>(o, want);
+    static std::atomic<int> slot{0};
+    const int qs = slot.fetch_add(1) % V6_QSLOTS;
     fate_score_v6_kernel<DPL, OVR, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
-                                                                    *work, *out, lay, ipc);
+                                                                    *work, *out, lay, qs);
     return 0;
 }
 

@@ -796,35 +796,48 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     }
 }
 
-// Items are handed to warps from a per-CTA queue of V6_IPC consecutive items
-// (shared-memory ticket counter): a warp that finishes a cheap item takes the
-// next one instead of idling until the slowest warp of its CTA is done, so
-// CTA slots are not held by finished warps (item costs vary several-fold with
-// the number of walked horizon levels).
-constexpr int V6_IPC = 8;  // default items per CTA (FATE_V6_IPC overrides, A/B only)
+// Work distribution: a persistent grid (every resident CTA slot once) whose
+// warps pull items from a global ticket counter, V6_FETCH items per ticket,
+// until the batch is exhausted: a warp that finishes a cheap item takes the
+// next one instead of holding a CTA slot idle (item costs vary several-fold
+// with the number of walked horizon levels, and consecutive items -- stages
+// of one scenario in index order -- have correlated costs).  Each launch uses
+// its own counter slot (host-side ring), and the last warp of a launch resets
+// the slot to zero, so a captured graph replays without a reset node.
+constexpr int V6_FETCH = 2;
+constexpr int V6_QSLOTS = 128;
+__device__ unsigned int g_v6_queue[2 * V6_QSLOTS];  // per slot: next ticket, warps done
 
 template <int DPL, bool OVR, int MINB>
 __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, fate_weights w,
                                                                   fate_windows win,
                                                                   fate_derived der, fate_state st,
                                                                   fate_work work, fate_out out,
-                                                                  V6Layout lay, int ipc) {
+                                                                  V6Layout lay, int qslot) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_next;
     const int wi = threadIdx.x >> 5, t = threadIdx.x & 31;
-    if (threadIdx.x == 0) s_next = 0;
-    __syncthreads();
-    const long long first = (long long)blockIdx.x * ipc;
-    const long long left = work.n_items - first;
-    const int n = left < ipc ? (int)left : ipc;
+    unsigned int* q = g_v6_queue + 2 * qslot;
+    const long long n = work.n_items;
     unsigned char* sb = smem_raw + lay.item_bytes * wi;
-    #pragma unroll 1
     for (;;) {
-        int i = 0;
-        if (t == 0) i = atomicAdd(&s_next, 1);
+        unsigned int i = 0;
+        if (t == 0) i = atomicAdd(q, (unsigned)V6_FETCH);
         i = __shfl_sync(0xffffffffu, i, 0);
-        if (i >= n) break;
-        v6_item<DPL, OVR>(b, w, win, der, st, work, out, lay, first + i, sb);
-        __syncwarp();  // the slice is reused by the next item
+        if ((long long)i >= n) break;
+        const long long i1 = (long long)i + V6_FETCH < n ? (long long)i + V6_FETCH : n;
+#pragma unroll 1
+        for (long long it = i; it < i1; ++it) {
+            v6_item<DPL, OVR>(b, w, win, der, st, work, out, lay, it, sb);
+            __syncwarp();  // the slice is reused by the next item
+        }
+    }
+    if (t == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(q + 1, 1u);
+        if (done == gridDim.x * (blockDim.x >> 5) - 1) {  // last warp of the launch
+            q[0] = 0u;
+            q[1] = 0u;
+            __threadfence();
+        }
     }
 }
