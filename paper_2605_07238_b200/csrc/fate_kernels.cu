@@ -779,6 +779,22 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
     if (rc) return rc;
     if (!out) return fail(FATE_EINVAL, "derived is NULL");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    {
+        // the v6 quotient tables, once per device (stream-ordered before any
+        // scoring launch that follows this prologue)
+        static std::atomic<unsigned long long> done{0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const unsigned long long bit = 1ull << (dev & 63);
+        if (!(done.load() & bit)) {
+            fate_v6_tables_kernel<<<(V6_DIVTAB + 127) / 128, 128, 0, s>>>();
+            g_launches++;
+            if ((rc = cuda_status("fate_v6_tables_kernel"))) return rc;
+            // one-time: make the tables visible to scoring launches on any stream
+            if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fate_v6_tables_kernel");
+            done.fetch_or(bit);
+        }
+    }
     if (bank->n_stages > 0) {
         const int threads = 128;
         const int blocks = (bank->n_stages + threads - 1) / threads;

@@ -192,6 +192,42 @@ __global__ void fate_template_fill_kernel(fate_bank b, fate_weights w, fate_wind
 }
 
 // ---------------------------------------------------------------------------
+// exact quotient tables (universal constants, one copy per device)
+// ---------------------------------------------------------------------------
+// n / 1000.0 for integer token counts n < V6_DIVTAB (prefix overlap,
+// costs.py:145; query_compute's prefill tokens, costs.py:92) and h / n for
+// the colocated-parent fraction with n <= V6_COLO_N (costs.py:163).  Filled
+// by fate_v6_tables_kernel with the same IEEE division the kernel would
+// execute, so a lookup returns the identical double; larger operands divide.
+constexpr int V6_DIVTAB = 4096;
+constexpr int V6_COLO_N = 64;
+__device__ double g_v6_div1000[V6_DIVTAB];
+__device__ double g_v6_colo[(V6_COLO_N + 1) * (V6_COLO_N + 2) / 2];
+
+__global__ void fate_v6_tables_kernel() {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < V6_DIVTAB) g_v6_div1000[i] = (double)i / 1000.0;
+    if (i <= V6_COLO_N) {
+        const int n = i;
+        for (int h = 0; h <= n; ++h)
+            g_v6_colo[n * (n + 1) / 2 + h] = n > 0 ? (double)h / (double)n : 0.0;
+    }
+}
+
+__device__ __forceinline__ double v6_div1000(long long n) {
+    return (n >= 0 && n < V6_DIVTAB) ? __ldg(&g_v6_div1000[n]) : (double)n / 1000.0;
+}
+
+// query_compute numerator/denominator order (costs.py:92-94), tabulated /1000
+__device__ __forceinline__ double v6_qc_value(long long stage_part, long long query_part,
+                                              double pcoef, double pscale, double decode,
+                                              double cplx, double speed) {
+    const double prefill = v6_div1000(stage_part + query_part) * pcoef * pscale;
+    const double x = (prefill + decode) * cplx;
+    return speed == 1.0 ? x : x / speed;  // x / 1.0 == x exactly
+}
+
+// ---------------------------------------------------------------------------
 // helpers
 // ---------------------------------------------------------------------------
 
@@ -242,7 +278,7 @@ __device__ __forceinline__ double v6_qc(const fate_bank& b, const fate_state& st
         const long long cc = cached_tokens(st.kappa + drow * it.cap4, st.kappa_n[drow], qg, it.m);
         qp = qp - cc > 0 ? qp - cc : 0;
     }
-    return qc_value(sp, qp, it.pcoef, it.pscale, it.decode, it.cplx, b.dev_speed[dv]);
+    return v6_qc_value(sp, qp, it.pcoef, it.pscale, it.decode, it.cplx, b.dev_speed[dv]);
 }
 
 // ---------------------------------------------------------------------------
@@ -700,7 +736,12 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         const double sw = s_sw[d];
         const double tr = s_tr[d];
         // 0 / n == +0.0 exactly: divide only when a parent is co-located
-        const double colo = (pa1 > pa0 && hit[j] > 0) ? (double)hit[j] / (double)(pa1 - pa0) : 0.0;
+        const int npar = pa1 - pa0;
+        const double colo =
+            (npar > 0 && hit[j] > 0)
+                ? (npar <= V6_COLO_N ? __ldg(&g_v6_colo[npar * (npar + 1) / 2 + hit[j]])
+                                     : (double)hit[j] / (double)npar)
+                : 0.0;
 
         // prefix_overlap_thousands (costs.py:127-145), integer-exact
         long long tokens = 0;
@@ -719,7 +760,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             }
         }
         const double prefix =
-            w.kappa_prefix * (tokens == 0 ? 0.0 : (double)tokens / 1000.0) * w.prefix_x;
+            w.kappa_prefix * (tokens == 0 ? 0.0 : v6_div1000(tokens)) * w.prefix_x;
 
         // _parallel_benefit (costs.py:181-201)
         const double full_total = sw + tr + here[j];
