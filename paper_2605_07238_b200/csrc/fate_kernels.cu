@@ -547,9 +547,11 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     // persistent grid: every resident CTA slot once (capped by the item count)
     static thread_local size_t occ_smem = ~size_t(0);
     static thread_local int occ_dev = -1, o = 0;
+    static thread_local const void* occ_fn = nullptr;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (occ_smem != smem || occ_dev != dev) {
+    const void* fn = (const void*)fate_score_v6_kernel<DPL, OVR, MINB>;
+    if (occ_smem != smem || occ_dev != dev || occ_fn != fn) {
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fate_score_v6_kernel<DPL, OVR, MINB>,
@@ -557,6 +559,7 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
         o = std::max(1, sms * std::max(1, per));
         occ_smem = smem;
         occ_dev = dev;
+        occ_fn = fn;
     }
     if (work->n_items > 0x7fffffffLL - 4 * 128 * V6_FETCH)
         return fail(FATE_ETOOBIG, "v6: too many items for the 32-bit ticket counter");
@@ -631,6 +634,9 @@ int launch_v6(const fate_bank* bank, const fate_weights* w, const fate_windows* 
         case 1:
             return ovr ? launch_v6_mb<DPL, true, 1>(bank, w, win, der, st, work, out, s)
                        : launch_v6_mb<DPL, false, 1>(bank, w, win, der, st, work, out, s);
+        case 7:
+            return ovr ? launch_v6_mb<DPL, true, 7>(bank, w, win, der, st, work, out, s)
+                       : launch_v6_mb<DPL, false, 7>(bank, w, win, der, st, work, out, s);
         case 6:
             return ovr ? launch_v6_mb<DPL, true, 6>(bank, w, win, der, st, work, out, s)
                        : launch_v6_mb<DPL, false, 6>(bank, w, win, der, st, work, out, s);
