@@ -603,8 +603,9 @@ int launch_v4_mb(const fate_bank* bank, const fate_weights* w, const fate_window
 }
 
 // register budget: CTAs per SM the register allocation must allow.  Measured
-// on B200 (profiles/): 8 for one device slot per lane (<= 64 registers), 6 for
-// two (<= 80).  FATE_MINB = 1 | 6 | 8 overrides for A/B runs.
+// on B200 (profiles/): 8 for one device slot per lane (<= 64 registers); for
+// two, 6 (<= 80) for v4/v5 and 7 (<= 72, no spills) for v6.  FATE_MINB =
+// 1 | 6 | 7 | 8 overrides for A/B runs.
 int v4_minb(int dpl) {
     static int v = -1;
     if (v < 0) {
@@ -630,7 +631,8 @@ int launch_v6(const fate_bank* bank, const fate_weights* w, const fate_windows* 
               const fate_derived* der, const fate_state* st, const fate_work* work,
               const fate_out* out, cudaStream_t s) {
     const bool ovr = bank->has_overrides != 0;
-    switch (v4_minb(DPL)) {
+    const char* e = getenv("FATE_MINB");
+    switch (e ? atoi(e) : (DPL == 1 ? 8 : 7)) {
         case 1:
             return ovr ? launch_v6_mb<DPL, true, 1>(bank, w, win, der, st, work, out, s)
                        : launch_v6_mb<DPL, false, 1>(bank, w, win, der, st, work, out, s);

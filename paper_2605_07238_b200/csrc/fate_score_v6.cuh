@@ -214,8 +214,13 @@ __global__ void fate_v6_tables_kernel() {
     }
 }
 
+// IEEE division kept out of line: for operands the tables and shortcuts do not
+// cover (rare), so each call site costs a call instead of an inlined
+// division sequence (the kernel is instruction-cache bound on D = 64 banks).
+__device__ __noinline__ double v6_div(double a, double b) { return a / b; }
+
 __device__ __forceinline__ double v6_div1000(long long n) {
-    return (n >= 0 && n < V6_DIVTAB) ? __ldg(&g_v6_div1000[n]) : (double)n / 1000.0;
+    return (n >= 0 && n < V6_DIVTAB) ? __ldg(&g_v6_div1000[n]) : v6_div((double)n, 1000.0);
 }
 
 // query_compute numerator/denominator order (costs.py:92-94), tabulated /1000
@@ -224,7 +229,7 @@ __device__ __forceinline__ double v6_qc_value(long long stage_part, long long qu
                                               double cplx, double speed) {
     const double prefill = v6_div1000(stage_part + query_part) * pcoef * pscale;
     const double x = (prefill + decode) * cplx;
-    return speed == 1.0 ? x : x / speed;  // x / 1.0 == x exactly
+    return speed == 1.0 ? x : v6_div(x, speed);  // x / 1.0 == x exactly
 }
 
 // ---------------------------------------------------------------------------
@@ -740,7 +745,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         const double colo =
             (npar > 0 && hit[j] > 0)
                 ? (npar <= V6_COLO_N ? __ldg(&g_v6_colo[npar * (npar + 1) / 2 + hit[j]])
-                                     : (double)hit[j] / (double)npar)
+                                     : v6_div((double)hit[j], (double)npar))
                 : 0.0;
 
         // prefix_overlap_thousands (costs.py:127-145), integer-exact
@@ -826,8 +831,8 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             #pragma unroll 1
             for (int k = 1; k < bound; ++k) {
                 // x / 1 == x and x / 2 == x * 0.5 exactly (both correctly rounded x/2)
-                const double q1 = k == 1 ? bb : bb / (double)k;
-                const double q2 = k == 1 ? hv * 0.5 : hv / (double)(k + 1);
+                const double q1 = k == 1 ? bb : v6_div(bb, (double)k);
+                const double q2 = k == 1 ? hv * 0.5 : v6_div(hv, (double)(k + 1));
                 const double reduction = q1 - q2;
                 psi[(long long)k * D + d] = w.lambda_r * (reduction - overhead) -
                                             w.lambda_q * wait - w.lambda_s * sw * w.state_scale -
