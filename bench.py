@@ -313,6 +313,53 @@ def time_e2e(torch, pipe, steps, warmup, world, device):
     return t0.elapsed_time(t1) / steps
 
 
+def measure_host_solve(bank, work, psi_host, n_inst: int = 16) -> dict:
+    """Host frontier solve of the first ``n_inst`` config-5 instances on the
+    GPU cost matrix (outside every timed region): the reference's solve
+    restated in Python vs the native ``fate_solve_frontier``, both at budget 0
+    (option enumeration + deterministic greedy -- a full search of a 25-stage,
+    32-device frontier does not finish in either), selections compared."""
+    import numpy as np
+
+    from paper_2605_07238_b200 import solver as native
+    from paper_2605_07238_b200.wf import frontier as MF
+
+    D = bank.scalars["n_devices"]
+    elig = bank.arrays["st_elig"]
+    sc = np.asarray(work.scen)
+    devs = tuple(f"d{j:02d}" for j in range(D))
+    t_py = t_nat = 0.0
+    same = True
+    n_cand = 0
+    for inst in range(n_inst):
+        cands, bounds = [], {}
+        for w in np.nonzero(sc == inst)[0]:
+            g = int(work.stage[w])
+            sid = f"s{g:08d}"
+            bounds[sid] = int(work.bounds[w])
+            m = int(elig[g])
+            base = int(work.psi_off[w])
+            for k in range(bounds[sid]):
+                for d in range(D):
+                    if m >> d & 1:
+                        cands.append(MF.Candidate(sid, k, devs[d], float(psi_host[base + k * D + d])))
+        prob = MF.FrontierProblem(tuple(cands), bounds, devs)
+        n_cand += len(cands)
+        t0 = time.perf_counter()
+        a = MF.solve_frontier(prob, budget_s=0.0)
+        t1 = time.perf_counter()
+        b = native.solve_frontier(prob, budget_s=0.0)
+        t2 = time.perf_counter()
+        t_py += t1 - t0
+        t_nat += t2 - t1
+        same &= (a.selected, a.objective.hex(), a.optimal) == (b.selected, b.objective.hex(),
+                                                               b.optimal)
+    return {"instances": n_inst, "candidates_per_instance": n_cand / n_inst, "budget_s": 0.0,
+            "python_ms_per_instance": 1e3 * t_py / n_inst,
+            "native_ms_per_instance": 1e3 * t_nat / n_inst, "identical": bool(same),
+            "note": "host solve timed separately (north star); reference semantics restated"}
+
+
 def cpu_sample_rate(bank, weights, states, work, target_s: float = 12.0, threads: int = 0):
     """The C oracle port of the reference scorer on a bounded sample of the
     workload's work items (first items in order), all host threads."""
@@ -465,6 +512,10 @@ def run_fate(args):
            "path": "fate_pipeline_capture/replay: 4 scenario-aligned chunks, H2D / scoring / "
                    "D2H overlapped on 3 streams, one CUDA-graph launch per step"}
 
+    host_solve = None
+    if rank == 0 and world == 1 and args.workload == "c5" and args.mode == "frontier":
+        host_solve = measure_host_solve(bank, work, out.psi.cpu().numpy())
+
     c4 = None
     if world == 1 and args.workload == "c5" and not args.no_c4:
         c4 = measure_c4(torch, device, args)
@@ -494,6 +545,8 @@ def run_fate(args):
         }
         if c4 is not None:
             line["c4_sweep"] = c4
+        if host_solve is not None:
+            line["host_solve"] = host_solve
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -246,6 +246,42 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
                const fate_derived* der, const fate_state* st, const fate_work* work,
                const fate_out* out, void* stream);
 
+/* ---- host frontier solve -------------------------------
+ * Native restatement of wfsched.planner.solve_frontier with its front half
+ * _stage_options and the deadline fallback _greedy_fallback
+ * (planner.py:101-234), same selection, objective bits, optimal flag and
+ * node count.  One problem = one FrontierProblem: stages in sorted(stage_id)
+ * order (only stages that have candidates), per stage its slots 0..bound-1,
+ * per slot the eligible devices ascending (device index = rank in
+ * sorted(device_ids)) with their Psi.  HOST memory. */
+typedef struct fate_frontier {
+    int32_t n_stages;
+    int32_t n_devices;              /* <= FATE_MAX_DEVICES */
+    const int32_t* slot_ptr;        /* [n_stages+1] into the slot rows */
+    const int32_t* cand_ptr;        /* [slot_ptr[n_stages]+1] into cand_* */
+    const int32_t* cand_dev;        /* device index, ascending within a slot */
+    const double* cand_psi;
+} fate_frontier;
+
+typedef struct fate_selection {
+    int32_t capacity;               /* entries of stage/slot/device (>= n_devices) */
+    int32_t n;                      /* selected (stage, slot, device), sorted */
+    int32_t* stage;
+    int32_t* slot;
+    int32_t* device;
+    double objective;
+    int32_t optimal;                /* 0: deadline hit, greedy fallback */
+    int32_t reserved;
+    int64_t nodes;                  /* FrontierSolution.nodes_explored */
+    int64_t n_options;              /* kept options over all stages */
+    double wall_s;
+} fate_selection;
+
+/* budget_s <= 0 times out at the first memo miss (the reference's zero
+ * budget); max_options <= 0 means 2^26. */
+int fate_solve_frontier(const fate_frontier* p, double budget_s, int64_t max_options,
+                        fate_selection* out);
+
 /* Device: count kernel launches issued by this library since load (for the
  * benchmark's gpu_launches evidence). */
 int64_t fate_launch_count(void);

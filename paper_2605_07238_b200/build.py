@@ -20,7 +20,8 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfate.so")
 SOURCES = [os.path.join(CSRC, "fate_kernels.cu"), os.path.join(CSRC, "fate_host.cpp"),
-           os.path.join(CSRC, "fate_synth.cpp"), os.path.join(CSRC, "fate_pipeline.cpp")]
+           os.path.join(CSRC, "fate_synth.cpp"), os.path.join(CSRC, "fate_pipeline.cpp"),
+           os.path.join(CSRC, "fate_solver.cpp")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-ffp-contract=off", "-I", INCLUDE]

@@ -131,11 +131,25 @@ class FateGpuPolicy:
 
     name = "fate"
 
-    def __init__(self, solver_budget_s: float = 0.25, scorer: GpuScorer | None = None):
+    def __init__(self, solver_budget_s: float = 0.25, scorer: GpuScorer | None = None,
+                 solver: str = "python"):
+        """``solver``: "python" = the restated reference solve (default: its
+        wall-clock behaviour matches the reference's), "native" =
+        ``fate_solve_frontier`` (same result whenever both finish or at a zero
+        budget; finishes more problems within a budget)."""
+        if solver not in ("python", "native"):
+            raise ValueError(f"unknown solver {solver!r}")
         self.solver_budget_s = solver_budget_s
         self.solver_stats = SolverStats()
         self.scorer = scorer or default_scorer()
         self.score_seconds = 0.0
+        self.solver = solver
+        if solver == "native":
+            from .solver import solve_frontier as native
+
+            self._solve = native
+        else:
+            self._solve = solve_frontier
 
     def plan_wave(self, state, frontier, dag, cost_model) -> list:
         t0 = time.perf_counter()
@@ -145,7 +159,7 @@ class FateGpuPolicy:
         if cost_model.weights.horizon == 0:
             return self._greedy_wave(wave, queries)
         problem = _problem_of(wave, cost_model)
-        solution = solve_frontier(problem, budget_s=self.solver_budget_s)
+        solution = self._solve(problem, budget_s=self.solver_budget_s)
         self.solver_stats.record(solution)
         chosen = self._fill_idle(solution.selected, problem, wave, state)
         if not chosen:

@@ -186,11 +186,16 @@ def check_c45_sampled(gpu: bool) -> int:
     return checked
 
 
-def check_c5_assign(gpu: bool) -> int:
+def check_c5_assign(gpu: bool, native_solver: bool = False) -> int:
     """Config-5 assignments: the host solve (budget 0, deterministic greedy) on
     the GPU/oracle cost matrix selects exactly what the reference's solve
-    selects on the reference's own cost matrix (tests/golden/c5_assign.json)."""
+    selects on the reference's own cost matrix (tests/golden/c5_assign.json).
+    ``native_solver`` solves with ``fate_solve_frontier`` instead of the
+    Python restatement."""
     from paper_2605_07238_b200.wf.frontier import Candidate, FrontierProblem, solve_frontier
+
+    if native_solver:
+        from paper_2605_07238_b200.solver import solve_frontier
 
     with open(os.path.join(G.GOLDEN, "c5_assign.json")) as fh:
         golden = json.load(fh)

@@ -150,9 +150,10 @@ def record_mismatches(rec, want: dict) -> list:
     return out
 
 
-def replay(run_meta: dict, arrays: dict, instance, config, scorer, seed: int = 0):
+def replay(run_meta: dict, arrays: dict, instance, config, scorer, seed: int = 0,
+           solver: str = "python"):
     chk = CheckingScorer(scorer, run_meta, arrays)
-    policy = FateGpuPolicy(scorer=chk)
+    policy = FateGpuPolicy(scorer=chk, solver=solver)
     rec = run(policy, instance, config, seed=seed)
     problems = list(chk.mismatches)
     if chk.i != len(run_meta["waves"]):
