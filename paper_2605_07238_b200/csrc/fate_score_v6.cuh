@@ -723,12 +723,20 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     double* psi = out.psi + work.psi_off[item];
     const double split = no_loc ? 0.0 : (bound > 1 ? c2.y : 0.0);
     const bool no_pre = w.ablation & FATE_NO_PREFIX;
-#pragma unroll
+    // One copy of the assembly code for both device slots (the loop is not
+    // unrolled; slot values are selected, not indexed): halves this phase's
+    // SASS for D > 32, which is instruction-cache bound.
+#define V6_PICK(x) (J ? x[DPL - 1] : x[0])
+#pragma unroll 1
     for (int j = 0; j < DPL; ++j) {
-        if (!live[j]) continue;
-        const int d = dv[j];
+        const bool J = DPL > 1 && j != 0;
+        if (!V6_PICK(live)) continue;
+        const int d = V6_PICK(dv);
         const long long orow = item * D + d;
-        if (!ok[j]) {
+        const double tail_j = V6_PICK(tail);
+        const double here_j = V6_PICK(here);
+        const int hit_j = V6_PICK(hit);
+        if (!V6_PICK(ok)) {
             const double qnan = __longlong_as_double(0x7ff8000000000000LL);
             #pragma unroll 1
             for (int k = 0; k < bound; ++k) psi[(long long)k * D + d] = qnan;
@@ -737,20 +745,20 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             if (out.completion) out.completion[orow] = qnan;
             continue;
         }
-        const double wait = py_max0(fr[j] - clock);
+        const double wait = py_max0(V6_PICK(fr) - clock);
         const double sw = s_sw[d];
         const double tr = s_tr[d];
         // 0 / n == +0.0 exactly: divide only when a parent is co-located
         const int npar = pa1 - pa0;
         const double colo =
-            (npar > 0 && hit[j] > 0)
-                ? (npar <= V6_COLO_N ? __ldg(&g_v6_colo[npar * (npar + 1) / 2 + hit[j]])
-                                     : v6_div((double)hit[j], (double)npar))
+            (npar > 0 && hit_j > 0)
+                ? (npar <= V6_COLO_N ? __ldg(&g_v6_colo[npar * (npar + 1) / 2 + hit_j])
+                                     : v6_div((double)hit_j, (double)npar))
                 : 0.0;
 
         // prefix_overlap_thousands (costs.py:127-145), integer-exact
         long long tokens = 0;
-        if (cache_reuse) tokens += it.Pv - cs[j];  // min(cached, P) = P - sp
+        if (cache_reuse) tokens += it.Pv - V6_PICK(cs);  // min(cached, P) = P - sp
         if (per_device_rows) {
             const long long row = it.dev_row0 + d;
             const int32_t* kap = st.kappa + row * it.cap4;
@@ -768,7 +776,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             w.kappa_prefix * (tokens == 0 ? 0.0 : v6_div1000(tokens)) * w.prefix_x;
 
         // _parallel_benefit (costs.py:181-201)
-        const double full_total = sw + tr + here[j];
+        const double full_total = sw + tr + here_j;
         double parallel = 0.0;
         if (R > 1 && !no_shard) {
             const bool self_idle = (idle_m >> d) & 1ull;
@@ -803,7 +811,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                     const double tot = s_sw[dev] + s_tr[dev] + ssum;
                     if (i == 0 || tot > worst) worst = tot;
                 }
-                const double overhead = w.shard_overhead_frac * here[j] * (double)(k - 1);
+                const double overhead = w.shard_overhead_frac * here_j * (double)(k - 1);
                 parallel = py_max0(full_total - worst - overhead);
             }
         }
@@ -819,13 +827,13 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                          + w.lambda_p * prefix_s * w.prefix_scale + w.lambda_r * par_s;
 
         if (out.sched) out.sched[orow] = S;
-        if (out.tail) out.tail[orow] = tail[j];
+        if (out.tail) out.tail[orow] = tail_j;
         if (out.completion) out.completion[orow] = wait + full_total;
-        psi[d] = S + tail[j];
+        psi[d] = S + tail_j;
 
         // _marginal_shard_score (costs.py:249-279)
         if (bound > 1) {
-            const double hv = here[j] > bb ? here[j] : bb;
+            const double hv = here_j > bb ? here_j : bb;
             const double overhead = w.shard_overhead_frac * bb;
             const double tr_m = no_loc ? 0.0 : tr;
             #pragma unroll 1
@@ -840,6 +848,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             }
         }
     }
+#undef V6_PICK
 }
 
 // Work distribution: a persistent grid (every resident CTA slot once) whose
