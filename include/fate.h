@@ -292,7 +292,9 @@ int64_t fate_launch_count(void);
  * (pin it for overlap), Psi / S / completion written to HOST memory.
  *
  * Host wire format: one fixed-size record per scenario (so any scenario range
- * is ONE contiguous copy), the loc rows, and one 16-byte record per item.
+ * is ONE contiguous copy), the loc rows as int8 device indices (-1 = None;
+ * D <= 64 always fits: a quarter of the int32 device-side bytes over PCIe),
+ * and one 16-byte record per item.
  * Scenario record, 16-byte aligned, FATE_SCEN_REC_BYTES(D, cap) bytes:
  *   [0]          double  clock               (fate_state.scen_clock)
  *   [8]          int64   loc_off             (fate_state.scen_loc_off)
@@ -316,7 +318,8 @@ typedef struct fate_host_batch {
     int32_t kappa_cap;
     int64_t n_loc;
     const void* scen_rec;           /* [S * FATE_SCEN_REC_BYTES(D, kappa_cap)] */
-    const int32_t* loc;             /* [n_loc]; scenario loc_off nondecreasing */
+    const int8_t* loc;              /* [n_loc] output_device index, -1 = None; scenario
+                                       loc_off nondecreasing */
     int32_t n_items;
     int32_t reserved;
     int64_t n_psi;                  /* entries of the Psi output */

@@ -17,8 +17,10 @@ void fate_internal_count_launches(long long n);
 
 // Scatter wire-format scenario records [s0, s1) and items [i0, i1) (device
 // copies of fate_host_batch) into the fate_state / fate_work SoA of dst.
+// Wire loc rows [l0, l1) (int8) are widened into dst->loc.
 int fate_internal_unpack(const void* rec, size_t rec_bytes, int s0, int s1, int D, int cap,
-                         const fate_item* items, int i0, int i1, const fate_state* dst,
-                         int32_t* w_scen, int32_t* w_stage, int64_t* w_psi_off, cudaStream_t s);
+                         const fate_item* items, int i0, int i1, const int8_t* loc8, int64_t l0,
+                         int64_t l1, const fate_state* dst, int32_t* w_scen, int32_t* w_stage,
+                         int64_t* w_psi_off, cudaStream_t s);
 
 #endif

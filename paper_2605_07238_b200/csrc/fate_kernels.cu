@@ -710,11 +710,23 @@ int check_weights(const fate_weights* w, const fate_windows* win) {
 }
 
 // Wire format -> SoA (fate_pipeline.cpp): blocks [0, n_s) scatter one scenario
-// record each (layout in fate.h), the remaining blocks scatter 128 items each.
+// record each (layout in fate.h), the next n_ib blocks 128 items each, the rest
+// widen 512 int8 loc entries each.
 __global__ void fate_unpack_kernel(const unsigned char* __restrict__ rec, size_t rb, int s0,
                                    int n_s, int D, int cap, const fate_item* __restrict__ items,
-                                   int i0, int n_i, fate_state dst, int32_t* w_scen,
+                                   int i0, int n_i, int n_ib, const int8_t* __restrict__ loc8,
+                                   long long l0, long long l1, fate_state dst, int32_t* w_scen,
                                    int32_t* w_stage, int64_t* w_psi_off) {
+    if ((int)blockIdx.x >= n_s + n_ib) {
+        const long long base = l0 + ((long long)blockIdx.x - n_s - n_ib) * 512;
+        int32_t* out = const_cast<int32_t*>(dst.loc);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const long long i = base + k * 128 + threadIdx.x;
+            if (i < l1) out[i] = loc8[i];
+        }
+        return;
+    }
     if ((int)blockIdx.x < n_s) {
         const int s = s0 + blockIdx.x;
         const unsigned char* r = rec + rb * s;
@@ -755,14 +767,17 @@ long long fate_internal_launches() { return g_launches.load(); }
 void fate_internal_count_launches(long long n) { g_launches += n; }
 
 int fate_internal_unpack(const void* rec, size_t rec_bytes, int s0, int s1, int D, int cap,
-                         const fate_item* items, int i0, int i1, const fate_state* dst,
-                         int32_t* w_scen, int32_t* w_stage, int64_t* w_psi_off, cudaStream_t s) {
+                         const fate_item* items, int i0, int i1, const int8_t* loc8, int64_t l0,
+                         int64_t l1, const fate_state* dst, int32_t* w_scen, int32_t* w_stage,
+                         int64_t* w_psi_off, cudaStream_t s) {
     const int n_s = s1 - s0, n_i = i1 - i0;
-    const unsigned blocks = (unsigned)(n_s + (n_i + 127) / 128);
+    const int n_ib = (n_i + 127) / 128;
+    const long long n_lb = (l1 - l0 + 511) / 512;
+    const unsigned blocks = (unsigned)(n_s + n_ib + n_lb);
     if (blocks == 0) return 0;
     fate_unpack_kernel<<<blocks, 128, 0, s>>>(static_cast<const unsigned char*>(rec), rec_bytes,
-                                               s0, n_s, D, cap, items, i0, n_i, *dst, w_scen,
-                                               w_stage, w_psi_off);
+                                               s0, n_s, D, cap, items, i0, n_i, n_ib, loc8, l0,
+                                               l1, *dst, w_scen, w_stage, w_psi_off);
     g_launches++;
     return cuda_status("fate_unpack_kernel");
 }

@@ -51,10 +51,10 @@ struct fate_pipeline {
         void* p = nullptr;
         size_t cap = 0;
     };
-    Buf rec, items, scen_inst, scen_clock, scen_loc_off, scen_done_level, loc, residency,
+    Buf rec, items, loc8, scen_inst, scen_clock, scen_loc_off, scen_done_level, loc, residency,
         dev_free, kappa_n, kappa, w_scen, w_stage, w_psi_off, psi, sched, completion;
     std::vector<Buf*> all() {
-        return {&rec, &items, &scen_inst, &scen_clock, &scen_loc_off, &scen_done_level, &loc,
+        return {&rec, &items, &loc8, &scen_inst, &scen_clock, &scen_loc_off, &scen_done_level, &loc,
                 &residency, &dev_free, &kappa_n, &kappa, &w_scen, &w_stage, &w_psi_off, &psi,
                 &sched, &completion};
     }
@@ -206,7 +206,7 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
         (rc = grow(p->scen_inst, 4 * (size_t)S)) || (rc = grow(p->scen_clock, 8 * (size_t)S)) ||
         (rc = grow(p->scen_loc_off, 8 * (size_t)S)) ||
         (rc = grow(p->scen_done_level, 4 * (size_t)S)) ||
-        (rc = grow(p->loc, 4 * (size_t)hb->n_loc)) ||
+        (rc = grow(p->loc, 4 * (size_t)hb->n_loc)) || (rc = grow(p->loc8, (size_t)hb->n_loc)) ||
         (rc = grow(p->residency, 4 * (size_t)S * D)) ||
         (rc = grow(p->dev_free, 8 * (size_t)S * D)) || (rc = grow(p->kappa_n, 4 * (size_t)S * D)) ||
         (rc = grow(p->kappa, 16 * (size_t)S * D * cap)) || (rc = grow(p->w_scen, 4 * (size_t)W)) ||
@@ -303,7 +303,7 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
         const Chunk& k = ch[c];
         const Copy h2d[] = {
             {drec + RB * k.sa, (const char*)hb->scen_rec + RB * k.sa, RB * (size_t)(k.sb - k.sa)},
-            {(int32_t*)p->loc.p + k.l0, hb->loc + k.l0, 4 * (size_t)(k.l1 - k.l0)},
+            {(int8_t*)p->loc8.p + k.l0, hb->loc + k.l0, (size_t)(k.l1 - k.l0)},
             {(fate_item*)p->items.p + k.i0, it + k.i0, 16 * (size_t)(k.i1 - k.i0)},
         };
         for (const Copy& cp : h2d) {
@@ -324,7 +324,8 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
             return cuda_fail(e, "fate_pipeline_score: H2D wait");
         mark(s);
         if ((rc = fate_internal_unpack(drec, (size_t)RB, k.sa, k.sb, D, cap,
-                                       (const fate_item*)p->items.p, k.i0, k.i1, &dst,
+                                       (const fate_item*)p->items.p, k.i0, k.i1,
+                                       (const int8_t*)p->loc8.p, k.l0, k.l1, &dst,
                                        (int32_t*)p->w_scen.p, (int32_t*)p->w_stage.p,
                                        (int64_t*)p->w_psi_off.p, s)))
             return rc;

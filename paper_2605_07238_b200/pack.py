@@ -477,7 +477,7 @@ def scen_rec_bytes(n_dev: int, cap: int) -> int:
 @dataclass
 class HostBatch:
     rec: np.ndarray      # uint8 [S * rec_bytes]
-    loc: np.ndarray      # int32 [n_loc]
+    loc: np.ndarray      # int8 [n_loc] (device index, -1 = None)
     items: np.ndarray    # ITEM_DTYPE [W]
     n_scenarios: int
     kappa_cap: int
@@ -507,5 +507,8 @@ def host_batch(states: PackedStates, work: WorkList, n_dev: int) -> HostBatch:
     items["scen"] = work.scen
     items["stage"] = work.stage
     items["psi_off"] = work.psi_off
-    return HostBatch(rec=rec.reshape(-1), loc=np.ascontiguousarray(a["loc"], dtype=np.int32),
+    loc = np.asarray(a["loc"])
+    if loc.size and (loc.max() >= n_dev or loc.min() < -1 or n_dev > 127):
+        raise ValueError("loc entries must be device indices < n_devices <= 127, or -1")
+    return HostBatch(rec=rec.reshape(-1), loc=np.ascontiguousarray(loc, dtype=np.int8),
                      items=items, n_scenarios=S, kappa_cap=cap, n_psi=work.n_psi)

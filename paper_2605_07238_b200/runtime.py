@@ -375,7 +375,7 @@ class HostPipeline:
         hb = host_batch(states, work, D)
         pin = (lambda a: torch.from_numpy(a).pin_memory())
         self.h_rec = pin(hb.rec)
-        self.h_loc = pin(hb.loc if hb.loc.size else np.zeros(1, np.int32))
+        self.h_loc = pin(hb.loc if hb.loc.size else np.zeros(1, np.int8))
         self.h_items = pin(hb.items.view(np.uint8))
         self.batch = abi.FateHostBatch(
             n_scenarios=hb.n_scenarios, kappa_cap=hb.kappa_cap, n_loc=int(hb.loc.size),

@@ -67,9 +67,8 @@ def main():
 
     cfg, bank, states, work, _ = bench.build_c5(0, 1, "frontier")
     dbank = runtime.DeviceBank(bank, cfg.weights, device=dev)
-    for chunks, streams, graph in ((1, 1, 0), (4, 1, 0), (6, 1, 0), (8, 1, 0), (4, 1, 1),
-                                   (5, 1, 1), (6, 1, 1), (8, 1, 1), (8, 2, 1), (12, 1, 1),
-                                   (16, 1, 1)):
+    for chunks, streams, graph in ((1, 1, 0), (4, 1, 0), (3, 1, 1), (4, 1, 1), (5, 1, 1),
+                                   (6, 1, 1), (8, 1, 1), (12, 1, 1)):
         pipe = runtime.HostPipeline(dbank, states, work, n_chunks=chunks, n_streams=streams,
                                     graph=bool(graph))
         ms = timed(pipe.run, reps=10)
