@@ -859,7 +859,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 // of one scenario in index order -- have correlated costs).  Each launch uses
 // its own counter slot (host-side ring), and the last warp of a launch resets
 // the slot to zero, so a captured graph replays without a reset node.
-constexpr int V6_FETCH = 2;
+constexpr int V6_FETCH = 2;  // items per ticket (FATE_V6_FETCH overrides, A/B only)
 constexpr int V6_QSLOTS = 128;
 __device__ unsigned int g_v6_queue[2 * V6_QSLOTS];  // per slot: next ticket, warps done
 
@@ -868,7 +868,8 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
                                                                   fate_windows win,
                                                                   fate_derived der, fate_state st,
                                                                   fate_work work, fate_out out,
-                                                                  V6Layout lay, int qslot) {
+                                                                  V6Layout lay, int qslot,
+                                                                  int fetch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int wi = threadIdx.x >> 5, t = threadIdx.x & 31;
     unsigned int* q = g_v6_queue + 2 * qslot;
@@ -876,10 +877,10 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
     unsigned char* sb = smem_raw + lay.item_bytes * wi;
     for (;;) {
         unsigned int i = 0;
-        if (t == 0) i = atomicAdd(q, (unsigned)V6_FETCH);
+        if (t == 0) i = atomicAdd(q, (unsigned)fetch);
         i = __shfl_sync(0xffffffffu, i, 0);
         if ((long long)i >= n) break;
-        const long long i1 = (long long)i + V6_FETCH < n ? (long long)i + V6_FETCH : n;
+        const long long i1 = (long long)i + fetch < n ? (long long)i + fetch : n;
 #pragma unroll 1
         for (long long it = i; it < i1; ++it) {
             v6_item<DPL, OVR>(b, w, win, der, st, work, out, lay, it, sb);
