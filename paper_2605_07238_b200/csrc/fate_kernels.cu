@@ -14,19 +14,12 @@
 // sequential += where the reference loops.  Parallelism is used only across
 // candidates, for gathers, and for order-free reductions (min/max/counts).
 //
-// Work decomposition (v1): one "item" = (scenario, stage v) owns TPI threads
-// (TPI = D rounded up to a warp), one thread per device d.  Items are packed
-// IPB per CTA.  Per item:
-//   A. all TPI threads fill the cache-aware query_compute table qc[d][q]
-//      in shared memory (costs.py:70-94);
-//   B. thread d: aware(d) = Neumaier sum of its row (= full-batch compute,
-//      costs.py:257 and :404), switch(d), transfer(d) (costs.py:107-125),
-//      idle flag (costs.py:190);
-//   C. one thread: base_best = min over eligible aware (costs.py:259) and the
-//      sorted idle-device list (costs.py:187-191);
-//   D. thread d: wait, colo, prefix overlap, parallel benefit (using other
-//      devices' qc rows for the split shards), S, tail over the horizon window,
-//      Psi(slot 0), Psi(slot k>=1), completion.
+// Work decomposition: one "item" = (scenario, stage v) is scored by one warp
+// (fate_score_v6.cuh, the production kernel; fate_score_v5.cuh is the previous
+// generation, kept for A/B).  This file holds the shared device helpers, the
+// prologue kernels of fate_prepare (mean_base, demand, split penalty, edge
+// terms, static tail tables, stage records, op templates), the wire-format
+// unpack kernel of the host pipeline, and the C ABI.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -120,22 +113,6 @@ __device__ __forceinline__ double qc_value(long long stage_part, long long query
     double prefill = (double)(stage_part + query_part) / 1000.0 * pcoef * pscale;
     const double x = (prefill + decode) * cplx;
     return speed == 1.0 ? x : x / speed;  // x / 1.0 == x exactly
-}
-
-struct ItemSmem {
-    double* qc;       // [D * Bmax]
-    double* aware;    // [D]
-    double* swc;      // [D]
-    double* trc;      // [D]
-    int* idle;        // [D] sorted eligible idle devices
-    int* misc;        // [4]: n_idle
-    double* bb;       // [1]
-};
-
-__host__ __device__ __forceinline__ size_t item_smem_bytes(int D, int Bmax) {
-    size_t doubles = (size_t)D * Bmax + 3 * (size_t)D + 1;
-    size_t ints = (size_t)D + 4;
-    return doubles * sizeof(double) + ((ints * sizeof(int) + 15) & ~size_t(15));
 }
 
 // ---------------------------------------------------------------------------
@@ -244,291 +221,7 @@ __global__ void fate_prepare_demand_kernel(fate_bank b, fate_windows win, fate_d
     out.demand[t] = dem;
 }
 
-// ---------------------------------------------------------------------------
-// main scoring kernel
-// ---------------------------------------------------------------------------
-
-template <int TPI>
-__global__ void __launch_bounds__(128) fate_score_kernel(fate_bank b, fate_weights w,
-                                                         fate_windows win, fate_derived der,
-                                                         fate_state st, fate_work work,
-                                                         fate_out out) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int IPB = 128 / TPI;
-    const int D = b.n_devices;
-    const int Bmax = b.max_queries;
-    const int lane_item = threadIdx.x / TPI;  // item slot in this CTA
-    const int t = threadIdx.x % TPI;          // thread within the item (= device in B/D)
-    const long long item = (long long)blockIdx.x * IPB + lane_item;
-    const bool live = item < work.n_items;
-
-    const size_t per_item = item_smem_bytes(D, Bmax);
-    unsigned char* base = smem_raw + per_item * lane_item;
-    ItemSmem sm;
-    sm.qc = reinterpret_cast<double*>(base);
-    sm.aware = sm.qc + (size_t)D * Bmax;
-    sm.swc = sm.aware + D;
-    sm.trc = sm.swc + D;
-    sm.bb = sm.trc + D;
-    sm.idle = reinterpret_cast<int*>(sm.bb + 1);
-    sm.misc = sm.idle + D;
-
-    // ---- item constants ------------------------------------------------------
-    int s = 0, v = 0, inst = 0, q0 = 0, nq = 0, m = -1, r = 0, R = 1, gv = -1, Pv = 0, Ov = 0;
-    uint64_t elig = 0;
-    double clock = 0.0, pcoef = 1.0, pscale = 1.0, decode = 0.0, cplx = 1.0, comm_v = 1.0;
-    bool cache_reuse = false;
-    const int32_t* loc_row = nullptr;
-    if (live) {
-        s = work.scen[item];
-        v = work.stage[item];
-        inst = st.scen_inst[s];
-        q0 = b.inst_query_off[inst];
-        nq = b.inst_n_queries[inst];
-        m = b.st_model[v];
-        r = b.st_role[v];
-        R = b.st_shard[v];
-        gv = b.st_group[v];
-        Pv = b.st_prompt[v];
-        Ov = b.st_out[v];
-        elig = b.st_elig[v];
-        clock = st.scen_clock[s];
-        pcoef = m >= 0 ? b.model_prefill[m] : 1.0;
-        const double dcoef = m >= 0 ? b.model_decode[m] : 0.0;
-        pscale = b.role_prefill[r];
-        cplx = b.role_cplx[r];
-        comm_v = b.role_comm[r];
-        decode = (double)Ov * dcoef * b.role_decode[r];
-        cache_reuse = (b.st_flags[v] & FATE_STAGE_CACHE_REUSE) && gv != -1;
-        loc_row = st.loc + st.scen_loc_off[s] - b.inst_stage_off[inst];
-    }
-    const int cap4 = st.kappa_cap * 4;
-    const long long dev_row0 = (long long)s * D;
-
-    // ---- A: cache-aware query_compute table ----------------------------------
-    if (live) {
-        for (int p = t; p < D * nq; p += TPI) {
-            const int d = p / nq, q = p - d * nq;
-            if (!((elig >> d) & 1ull)) continue;
-            const int32_t* kap = st.kappa + (dev_row0 + d) * cap4;
-            const int kn = st.kappa_n[dev_row0 + d];
-            long long sp = Pv, qp = b.q_prompt[q0 + q];
-            if (cache_reuse) {
-                const long long c = cached_tokens(kap, kn, gv, m);
-                sp = sp - c > 0 ? sp - c : 0;
-            }
-            const int qg = b.q_group[q0 + q];
-            if (qg != -1) {
-                const long long c = cached_tokens(kap, kn, qg, m);
-                qp = qp - c > 0 ? qp - c : 0;
-            }
-            sm.qc[d * Bmax + q] = qc_value(sp, qp, pcoef, pscale, decode, cplx, b.dev_speed[d]);
-        }
-    }
-    __syncthreads();
-
-    // ---- B: per-device sums, switch, transfer --------------------------------
-    const int d = t;
-    const bool dev_ok = live && d < D && ((elig >> d) & 1ull);
-    if (dev_ok) {
-        PySum acc;
-        for (int q = 0; q < nq; ++q) acc.add(sm.qc[d * Bmax + q]);
-        sm.aware[d] = acc.result();
-        const int res = st.residency[dev_row0 + d];
-        sm.swc[d] = (m < 0 || res == m) ? 0.0 : b.model_switch[m] * w.switch_x;
-        double tr = 0.0;
-        for (int e = b.par_ptr[v]; e < b.par_ptr[v + 1]; ++e) {
-            const int L = loc_row[b.par_idx[e]];
-            if (L < 0 || L == d) continue;
-            tr += b.beta[(size_t)L * D + d] * der.edge_sigma[e];
-        }
-        sm.trc[d] = tr * w.transfer_x;
-    }
-    __syncthreads();
-
-    // ---- C: base_best and the sorted idle list --------------------------------
-    if (live && t == 0) {
-        double bb = 0.0;
-        bool first = true;
-        int n_idle = 0;
-        const double limit = clock + 1e-12;
-        for (int e = 0; e < D; ++e) {
-            if (!((elig >> e) & 1ull)) continue;
-            const double a = sm.aware[e];
-            if (first || a < bb) bb = a;
-            first = false;
-            if (st.dev_free[dev_row0 + e] <= limit) sm.idle[n_idle++] = e;
-        }
-        sm.bb[0] = bb;
-        sm.misc[0] = n_idle;
-    }
-    __syncthreads();
-
-    if (!(live && d < D)) return;  // no barriers below
-    const int n_elig = __popcll(elig);
-    const int bound = (w.ablation & FATE_NO_SHARD) ? 1 : (R < n_elig ? R : n_elig);
-    if (!dev_ok) {
-        // ineligible device: no candidate; NaN marks the hole in the dense rows
-        const double qnan = __longlong_as_double(0x7ff8000000000000LL);
-        double* psi = out.psi + work.psi_off[item];
-        for (int k = 0; k < bound; ++k) psi[(long long)k * D + d] = qnan;
-        const long long orow = item * D + d;
-        if (out.sched) out.sched[orow] = qnan;
-        if (out.tail) out.tail[orow] = qnan;
-        if (out.completion) out.completion[orow] = qnan;
-        return;
-    }
-
-    // ---- D: per-candidate terms ------------------------------------------------
-    const double free_d = st.dev_free[dev_row0 + d];
-    const double wait = py_max0(free_d - clock);
-    const double sw = sm.swc[d];
-    const double tr = sm.trc[d];
-    const double here = sm.aware[d];
-    const bool no_loc = w.ablation & FATE_NO_LOCALITY;
-    const bool no_pre = w.ablation & FATE_NO_PREFIX;
-    const bool no_shard = w.ablation & FATE_NO_SHARD;
-
-    // colo (costs.py:160-165): located-on-d parents over ALL parents
-    const int pa0 = b.par_ptr[v], pa1 = b.par_ptr[v + 1];
-    double colo = 0.0;
-    if (pa1 > pa0) {
-        int hit = 0;
-        for (int e = pa0; e < pa1; ++e) hit += loc_row[b.par_idx[e]] == d;
-        colo = (double)hit / (double)(pa1 - pa0);
-    }
-
-    // prefix_overlap_thousands (costs.py:127-145): integer-exact token sum
-    const int32_t* kap = st.kappa + (dev_row0 + d) * cap4;
-    const int kn = st.kappa_n[dev_row0 + d];
-    long long tokens = 0;
-    if (cache_reuse) {
-        const long long c = cached_tokens(kap, kn, gv, m);
-        tokens += c < Pv ? c : Pv;
-    }
-    for (int q = 0; q < nq; ++q) {
-        const int qg = b.q_group[q0 + q];
-        if (qg == -1) continue;
-        const long long c = cached_tokens(kap, kn, qg, m);
-        const long long qp = b.q_prompt[q0 + q];
-        tokens += c < qp ? c : qp;
-    }
-    const double prefix = w.kappa_prefix * ((double)tokens / 1000.0) * w.prefix_x;
-
-    // _parallel_benefit (costs.py:181-201) with _even_split (costs.py:419-428)
-    const double full_total = sw + tr + here;
-    double parallel = 0.0;
-    if (R > 1 && !no_shard) {
-        const int n_idle = sm.misc[0];
-        const bool self_idle = free_d <= clock + 1e-12;
-        const int others = n_idle - (self_idle ? 1 : 0);
-        const int k = R < 1 + others ? R : 1 + others;
-        if (k > 1) {
-            double worst = 0.0;
-            int start = 0, j = 0;
-            for (int i = 0; i < k; ++i) {
-                int dev = d;
-                if (i > 0) {
-                    while (sm.idle[j] == d) ++j;
-                    dev = sm.idle[j++];
-                }
-                const int size = nq / k + (i < nq % k ? 1 : 0);
-                PySum acc;
-                for (int q = start; q < start + size; ++q) acc.add(sm.qc[dev * Bmax + q]);
-                const double tot = sm.swc[dev] + sm.trc[dev] + acc.result();
-                if (i == 0 || tot > worst) worst = tot;
-                start += size;
-            }
-            const double overhead = w.shard_overhead_frac * here * (double)(k - 1);
-            parallel = py_max0(full_total - worst - overhead);
-        }
-    }
-
-    // sched_score (costs.py:210-231)
-    const double tr_s = no_loc ? 0.0 : tr;
-    const double colo_s = no_loc ? 0.0 : colo;
-    const double prefix_s = no_pre ? 0.0 : prefix;
-    const double par_s = no_shard ? 0.0 : parallel;
-    const double S = -w.lambda_q * wait - w.lambda_s * sw * w.state_scale
-                     - w.lambda_tr * tr_s * w.locality_scale + w.lambda_c * colo_s * w.locality_scale
-                     + w.lambda_p * prefix_s * w.prefix_scale + w.lambda_r * par_s;
-
-    // tail_value (costs.py:281-352)
-    double tail = 0.0;
-    const int H = w.eff_horizon;
-    if (H > 1) {
-        const int res = st.residency[dev_row0 + d];
-        const bool displaces = res != -1 && res != m;
-        const bool no_same = w.ablation & FATE_NO_SAME_MODEL;
-        const int L = win.levels;
-        for (int l = 1; l < H; ++l) {
-            const long long lo = win.ptr[(long long)v * L + (l - 1)];
-            const long long hi = win.ptr[(long long)v * L + l];
-            if (hi == lo) continue;
-            double aff = 0.0;
-            for (long long i = lo; i < hi; ++i) {
-                const int x = win.idx[i];
-                const int mx = b.st_model[x];
-                if (!no_same && mx != -1) {
-                    if (mx == m) {
-                        aff += w.lambda_s * b.model_switch[mx] * w.switch_x * w.state_scale;
-                    } else if (displaces && mx == res) {
-                        aff -= w.lambda_s * b.model_switch[mx] * w.switch_x * w.state_scale;
-                    }
-                }
-                const int gx = b.st_group[x];
-                if (!no_pre && gx != -1 && gx == gv) {
-                    const int Px = b.st_prompt[x];
-                    const int shared = Pv < Px ? Pv : Px;
-                    aff += w.lambda_p * w.kappa_prefix * (double)shared / 1000.0 * w.prefix_x *
-                           w.prefix_scale;
-                }
-                if (!no_loc) {
-                    for (int e = b.par_ptr[x]; e < b.par_ptr[x + 1]; ++e) {
-                        const int p = b.par_idx[e];
-                        if (p == v) continue;
-                        const int Lp = loc_row[p];
-                        if (Lp < 0 || Lp == d) continue;
-                        if (b.has_overrides) {
-                            aff -= w.lambda_tr * b.beta[(size_t)Lp * D + d] * der.edge_sigma[e] *
-                                   w.transfer_x * w.locality_scale;
-                        } else {
-                            aff -= der.edge_term[e];
-                        }
-                    }
-                }
-            }
-            const double dem = der.demand[(long long)v * L + (l - 1)];
-            tail += w.gamma_pow[l] * (aff / (double)(hi - lo) + w.demand_coeff * dem);
-        }
-    }
-
-    const long long orow = item * D + d;
-    if (out.sched) out.sched[orow] = S;
-    if (out.tail) out.tail[orow] = tail;
-    if (out.completion) out.completion[orow] = wait + full_total;
-
-    double* psi = out.psi + work.psi_off[item];
-    psi[d] = S + tail;
-
-    // _marginal_shard_score (costs.py:249-279), slots 1..bound-1
-    if (bound > 1) {
-        const double bb = sm.bb[0];
-        const double hi_v = here > bb ? here : bb;
-        const double overhead = w.shard_overhead_frac * bb;
-        const double tr_m = no_loc ? 0.0 : tr;
-        const double split = no_loc ? 0.0 : der.split_penalty[v];
-        for (int k = 1; k < bound; ++k) {
-            const double reduction = bb / (double)k - hi_v / (double)(k + 1);
-            psi[(long long)k * D + d] = w.lambda_r * (reduction - overhead) - w.lambda_q * wait -
-                                        w.lambda_s * sw * w.state_scale -
-                                        w.lambda_tr * (tr_m + split) * w.locality_scale;
-        }
-    }
-}
-
-#include "fate_score_v3.cuh"
-#include "fate_score_v4.cuh"
+#include "fate_prologue.cuh"
 #include "fate_score_v5.cuh"
 #include "fate_score_v6.cuh"
 
@@ -595,26 +288,11 @@ int launch_v5_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     return 0;
 }
 
-template <int DPL, int MINB>
-int launch_v4_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
-                 const fate_derived* der, const fate_state* st, const fate_work* work,
-                 const fate_out* out, cudaStream_t s) {
-    const size_t smem = v4_item_bytes(bank->n_devices, bank->max_queries, win->max_level_ops) * 4;
-    if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v4 shared-memory footprint too large");
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fate_score_v4_kernel<DPL, MINB>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const unsigned blocks = (unsigned)((work->n_items + 3) / 4);
-    fate_score_v4_kernel<DPL, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st, *work,
-                                                               *out);
-    return 0;
-}
-
 // register budget: CTAs per SM the register allocation must allow.  Measured
 // on B200 (profiles/): 8 for one device slot per lane (<= 64 registers); for
 // two, 6 (<= 80) for v4/v5 and 7 (<= 72, no spills) for v6.  FATE_MINB =
 // 1 | 6 | 7 | 8 overrides for A/B runs.
-int v4_minb(int dpl) {
+int v5_minb(int dpl) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FATE_MINB");
@@ -627,7 +305,7 @@ template <int DPL>
 int launch_v5(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
               const fate_derived* der, const fate_state* st, const fate_work* work,
               const fate_out* out, cudaStream_t s) {
-    switch (v4_minb(DPL)) {
+    switch (v5_minb(DPL)) {
         case 1: return launch_v5_mb<DPL, 1>(bank, w, win, der, st, work, out, s);
         case 6: return launch_v5_mb<DPL, 6>(bank, w, win, der, st, work, out, s);
         default: return launch_v5_mb<DPL, 8>(bank, w, win, der, st, work, out, s);
@@ -656,44 +334,15 @@ int launch_v6(const fate_bank* bank, const fate_weights* w, const fate_windows* 
     }
 }
 
-template <int DPL>
-int launch_v4(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
-              const fate_derived* der, const fate_state* st, const fate_work* work,
-              const fate_out* out, cudaStream_t s) {
-    switch (v4_minb(DPL)) {
-        case 6: return launch_v4_mb<DPL, 6>(bank, w, win, der, st, work, out, s);
-        case 8: return launch_v4_mb<DPL, 8>(bank, w, win, der, st, work, out, s);
-        default: return launch_v4_mb<DPL, 1>(bank, w, win, der, st, work, out, s);
-    }
-}
-
-template <int G>
-int launch_v3(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
-              const fate_derived* der, const fate_state* st, const fate_work* work,
-              const fate_out* out, cudaStream_t s) {
-    constexpr int IPB = 128 / G;
-    const size_t smem = v3_item_bytes(bank->n_devices, bank->max_queries, G, win->max_level_ops) * IPB;
-    if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v3 shared-memory footprint too large");
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fate_score_v3_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    const unsigned blocks = (unsigned)((work->n_items + IPB - 1) / IPB);
-    fate_score_v3_kernel<G><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st, *work, *out);
-    return 0;
-}
-
-// Kernel generation (A/B benchmarking only): FATE_SCORE_KERNEL=v1|v3|v4|v5,
-// default v6 (which needs the stage records and op templates; without them
-// the library falls back to v5, the previous production kernel).
+// Kernel generation: v6 (production) needs the stage records and op templates
+// of fate_prepare; without them -- or with FATE_SCORE_KERNEL=v5 (A/B only) --
+// the previous production kernel v5 runs.  Generations v1-v4 live in the git
+// history (profiles/README.md has their measurements).
 int kernel_gen() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FATE_SCORE_KERNEL");
-        v = (e && strcmp(e, "v1") == 0)   ? 1
-            : (e && strcmp(e, "v3") == 0) ? 3
-            : (e && strcmp(e, "v4") == 0) ? 4
-            : (e && strcmp(e, "v5") == 0) ? 5
-                                          : 6;
+        v = (e && strcmp(e, "v5") == 0) ? 5 : 6;
     }
     return v;
 }
@@ -900,45 +549,15 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
     if (work->n_items <= 0) return 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int D = bank->n_devices;
-    const size_t per_item = item_smem_bytes(D, bank->max_queries);
     const bool v6_ready = der->stage_rec && (win->levels == 0 || (der->tmpl_ptr && der->tmpl));
     if (kernel_gen() == 6 && v6_ready) {
         rc = D <= 32 ? launch_v6<1>(bank, w, win, der, st, work, out, s)
                      : launch_v6<2>(bank, w, win, der, st, work, out, s);
-        if (rc) return rc;
-    } else if (kernel_gen() >= 5) {
+    } else {
         rc = D <= 32 ? launch_v5<1>(bank, w, win, der, st, work, out, s)
                      : launch_v5<2>(bank, w, win, der, st, work, out, s);
-        if (rc) return rc;
-    } else if (kernel_gen() == 4) {
-        rc = D <= 32 ? launch_v4<1>(bank, w, win, der, st, work, out, s)
-                     : launch_v4<2>(bank, w, win, der, st, work, out, s);
-        if (rc) return rc;
-    } else if (kernel_gen() == 3) {
-        rc = D <= 32 ? launch_v3<32>(bank, w, win, der, st, work, out, s)
-                     : launch_v3<64>(bank, w, win, der, st, work, out, s);
-        if (rc) return rc;
-    } else if (D <= 32) {
-        constexpr int TPI = 32, IPB = 128 / TPI;
-        const size_t smem = per_item * IPB;
-        if (smem > 48 * 1024) {
-            cudaFuncSetAttribute(fate_score_kernel<TPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        }
-        const unsigned blocks = (unsigned)((work->n_items + IPB - 1) / IPB);
-        fate_score_kernel<TPI><<<blocks, TPI * IPB, smem, s>>>(*bank, *w, *win, *der, *st, *work,
-                                                               *out);
-    } else {
-        constexpr int TPI = 64, IPB = 128 / TPI;
-        const size_t smem = per_item * IPB;
-        if (smem > 48 * 1024) {
-            cudaFuncSetAttribute(fate_score_kernel<TPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        }
-        const unsigned blocks = (unsigned)((work->n_items + IPB - 1) / IPB);
-        fate_score_kernel<TPI><<<blocks, TPI * IPB, smem, s>>>(*bank, *w, *win, *der, *st, *work,
-                                                               *out);
     }
+    if (rc) return rc;
     g_launches++;
     return cuda_status("fate_score_kernel");
 }
