@@ -859,7 +859,6 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 // of one scenario in index order -- have correlated costs).  Each launch uses
 // its own counter slot (host-side ring), and the last warp of a launch resets
 // the slot to zero, so a captured graph replays without a reset node.
-constexpr int V6_FETCH = 2;  // items per ticket (FATE_V6_FETCH overrides, A/B only)
 constexpr int V6_QSLOTS = 128;
 __device__ unsigned int g_v6_queue[2 * V6_QSLOTS];  // per slot: next ticket, warps done
 
@@ -875,12 +874,24 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
     unsigned int* q = g_v6_queue + 2 * qslot;
     const long long n = work.n_items;
     unsigned char* sb = smem_raw + lay.item_bytes * wi;
+    // fetch > 0: fixed items per ticket; fetch == 0: guided -- a ticket takes
+    // 1/(4 * warps) of what the warp last saw remaining (at least one), so
+    // early tickets are large (few atomics) and late ones single items (tail
+    // balance)
+    const long long n_warps = (long long)gridDim.x * (blockDim.x >> 5);
+    long long seen = 0;
     for (;;) {
+        long long take = fetch;
+        if (fetch == 0) {
+            take = (n - seen) / (4 * n_warps);
+            take = take < 1 ? 1 : (take > 16 ? 16 : take);
+        }
         unsigned int i = 0;
-        if (t == 0) i = atomicAdd(q, (unsigned)fetch);
+        if (t == 0) i = atomicAdd(q, (unsigned)take);
         i = __shfl_sync(0xffffffffu, i, 0);
+        seen = (long long)i + take;
         if ((long long)i >= n) break;
-        const long long i1 = (long long)i + fetch < n ? (long long)i + fetch : n;
+        const long long i1 = (long long)i + take < n ? (long long)i + take : n;
 #pragma unroll 1
         for (long long it = i; it < i1; ++it) {
             v6_item<DPL, OVR>(b, w, win, der, st, work, out, lay, it, sb);
