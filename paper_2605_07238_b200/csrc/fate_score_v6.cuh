@@ -852,7 +852,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 }
 
 // Work distribution: a persistent grid (every resident CTA slot once) whose
-// warps pull items from a global ticket counter, V6_FETCH items per ticket,
+// warps pull items from a global ticket counter (ticket sizes: see below),
 // until the batch is exhausted: a warp that finishes a cheap item takes the
 // next one instead of holding a CTA slot idle (item costs vary several-fold
 // with the number of walked horizon levels, and consecutive items -- stages
