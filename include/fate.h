@@ -197,6 +197,14 @@ typedef struct fate_derived {
                                        (v, l) the reference's tail op sequence
                                        (costs.py:307-348), edge entries resolved per
                                        scenario by parent location */
+    int32_t* tok_vals;              /* [n_stages*4] up to 3 partial-hit token counts t
+                                       (0 < t < P(v): prompts of keep_cache stages of v's
+                                       prefix group, the values state.py:236-247 seeds)
+                                       and their count */
+    double* tok_sums;               /* [n_stages*9] Neumaier sums (full batch, k=2 shard 0,
+                                       shard 1) of the row with stage part P(v) - t, per t;
+                                       valid under FATE_BANK_UNIFORM_SPEED without query
+                                       prefix groups (costs.py:257, :404-405) */
 } fate_derived;
 
 /* Outputs.  psi: per item bound(v)*D entries, slot-major, NaN where the

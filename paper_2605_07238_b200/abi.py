@@ -71,7 +71,7 @@ class FateWindows(C.Structure):
 class FateDerived(C.Structure):
     _fields_ = [(n, _p) for n in ("mean_base", "demand", "split_penalty", "edge_sigma",
                                   "edge_term", "row_sums", "inst_qgroups", "tail_sum", "tail_static",
-                                  "stage_rec", "tmpl_ptr", "tmpl")]
+                                  "stage_rec", "tmpl_ptr", "tmpl", "tok_vals", "tok_sums")]
 
 
 class FateOut(C.Structure):

@@ -481,6 +481,12 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
         fate_prepare_stage_kernel<<<blocks, threads, 0, s>>>(*bank, *w, *out);
         g_launches++;
         if ((rc = cuda_status("fate_prepare_stage_kernel"))) return rc;
+        if (out->tok_vals && out->tok_sums) {
+            if (!out->inst_qgroups) return fail(FATE_EINVAL, "token classes need inst_qgroups");
+            fate_prepare_tok_kernel<<<blocks, threads, 0, s>>>(*bank, *out);
+            g_launches++;
+            if ((rc = cuda_status("fate_prepare_tok_kernel"))) return rc;
+        }
         if (out->stage_rec) {
             if (!out->split_penalty || !out->inst_qgroups)
                 return fail(FATE_EINVAL, "stage records need split_penalty and inst_qgroups");

@@ -31,7 +31,11 @@
 
 constexpr int V6_KT = 4;               // shard counts k <= V6_KT: shard sums tabulated
 constexpr int V6_RCAP = 8;             // dynamic classes with a shared-memory row
-constexpr int V6_SLOTS = V6_RCAP + 2;  // table slots: 0 = static A, 1 = static B, 2+ = rows
+constexpr int V6_NTOK = 3;             // tabulated partial-hit classes per stage
+constexpr int V6_ROW0 = 2 + V6_NTOK;   // first dynamic-row slot
+// table slots: 0 = static A (sp = P), 1 = static B (sp = 0), 2..4 = tabulated
+// partial hits (sp = P - t), V6_ROW0+ = dynamic rows
+constexpr int V6_SLOTS = V6_RCAP + V6_ROW0;
 constexpr int V6_KEY_ALWAYS = 999;     // op applied on every device (same-model, prefix)
 constexpr int V6_KEY_MODEL = 1000;     // op key >= this: displacement op of model key-1000
 constexpr int V6_KEY_SIGMA = 2000;     // OVR edge op: key-2000 = location, val = sigma
@@ -394,7 +398,12 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             }
         }
     }
-    const double rsum = t < 6 ? der.row_sums[(size_t)v * 6 + t] : 0.0;  // static-class sums
+    // static-class sums: lanes 0-5 row_sums (A, B), lanes 6-14 tok_sums (T0..T2)
+    const double rsum = t < 6    ? der.row_sums[(size_t)v * 6 + t]
+                        : t < 15 ? (der.tok_sums ? der.tok_sums[(size_t)v * 9 + t - 6] : 0.0)
+                                 : 0.0;
+    const int4 tokv = der.tok_vals ? __ldg(reinterpret_cast<const int4*>(der.tok_vals) + v)
+                                   : make_int4(0, 0, 0, 0);
 
     // ---- P0: per-device stage part, switch; v's parents --------------------------------------
     int cs[DPL], hit[DPL];
@@ -501,20 +510,28 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     const bool kb_ok = kb >= 2 && kb <= V6_KT;
     const bool ki_ok = ki != kb && ki >= 2 && ki <= V6_KT;
     const int per = 1 + (kb_ok ? kb : 0) + (ki_ok ? ki : 0);
-    // static classes: representatives with sp == P (A) and sp == 0 < P (B)
-    unsigned long long am = 0ull, bm = 0ull;
+    // static classes: representatives with sp == P (A), sp == 0 < P (B), and
+    // sp == P - t for a tabulated partial-hit token count t (T0..T2)
+    unsigned long long am = 0ull, bm = 0ull, tm[V6_NTOK] = {0ull, 0ull, 0ull};
     if (uniform && !per_device_rows && kb <= 2 && ki <= 2) {
 #pragma unroll
         for (int j = 0; j < DPL; ++j) {
             const bool r0 = ok[j] && rep[j] == dv[j];
             am |= (unsigned long long)__ballot_sync(FULL, r0 && cs[j] == it.Pv) << (32 * j);
             bm |= (unsigned long long)__ballot_sync(FULL, r0 && cs[j] == 0 && it.Pv > 0) << (32 * j);
+            const int tt = it.Pv - cs[j];  // cached tokens behind this class
+            const bool part = r0 && cs[j] > 0 && cs[j] < it.Pv;
+            tm[0] |= (unsigned long long)__ballot_sync(FULL, part && tokv.w > 0 && tt == tokv.x) << (32 * j);
+            tm[1] |= (unsigned long long)__ballot_sync(FULL, part && tokv.w > 1 && tt == tokv.y) << (32 * j);
+            tm[2] |= (unsigned long long)__ballot_sync(FULL, part && tokv.w > 2 && tt == tokv.z) << (32 * j);
         }
     }
-    const unsigned long long dyn_m = rep_m & ~am & ~bm;  // representatives of dynamic classes
+    // representatives of dynamic classes
+    const unsigned long long dyn_m = rep_m & ~am & ~bm & ~tm[0] & ~tm[1] & ~tm[2];
     const int n_dyn = __popcll(dyn_m);
     const int n_rows = n_dyn < V6_RCAP ? n_dyn : V6_RCAP;
-    // table slot of each device's class: 0 = A, 1 = B, 2 + row slot, -1 = direct
+    // table slot of each device's class: 0 = A, 1 = B, 2..4 = T0..T2,
+    // V6_ROW0 + row slot, -1 = direct
 #pragma unroll
     for (int j = 0; j < DPL; ++j) {
         if (!ok[j]) continue;
@@ -522,17 +539,22 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         int slot;
         if (am & rb) slot = 0;
         else if (bm & rb) slot = 1;
+        else if (tm[0] & rb) slot = 2;
+        else if (tm[1] & rb) slot = 3;
+        else if (tm[2] & rb) slot = 4;
         else {
             const int r = __popcll(dyn_m & low_mask(rep[j]));
-            slot = r < V6_RCAP ? 2 + r : -1;
+            slot = r < V6_RCAP ? V6_ROW0 + r : -1;
             if (rep[j] == dv[j] && r < V6_RCAP) s_rowdev[r] = dv[j];
         }
         s_cslot[dv[j]] = slot;
     }
-    if (t < 6) {
-        // lane t holds row_sums[v][t]: class si = t / 3, entry e = t % 3 (full, shard 0, 1)
+    if (t < 15) {
+        // lane t holds the sums of static class si = t / 3 (A, B, T0, T1, T2),
+        // entry e = t % 3 (full, k=2 shard 0, shard 1)
         const int si = t / 3, e = t - 3 * si;
-        if (si == 0 ? am != 0ull : bm != 0ull) {
+        const unsigned long long cm = si == 0 ? am : si == 1 ? bm : tm[si - 2];
+        if (cm != 0ull) {
             if (e == 0) {
                 s_aware[si] = rsum;
             } else {
@@ -555,7 +577,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         const int r = p / per;
         int j = p - r * per;
         const double* row = s_rows + r * Bmax;
-        const int slot = 2 + r;
+        const int slot = V6_ROW0 + r;
         PySum acc;
         if (j == 0) {
             #pragma unroll 1
@@ -804,8 +826,8 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                         PySum acc;
                         #pragma unroll 1
                         for (int q = lo; q < hi; ++q)
-                            acc.add(slot >= 2 ? s_rows[(slot - 2) * Bmax + q]
-                                              : v6_qc(b, st, it, s_key, dev, q));
+                            acc.add(slot >= V6_ROW0 ? s_rows[(slot - V6_ROW0) * Bmax + q]
+                                                    : v6_qc(b, st, it, s_key, dev, q));
                         ssum = acc.result();
                     }
                     const double tot = s_sw[dev] + s_tr[dev] + ssum;

@@ -252,6 +252,8 @@ class DeviceBank:
         n_static = n * self.levels * (packed.scalars["n_models"] + 1)
         self.tail_static = torch.empty(max(n_static, 1), **f64)
         self.stage_rec = torch.empty(max(n, 1) * 112, dtype=torch.uint8, device=self.device)
+        self.tok_vals = torch.empty(max(n, 1) * 4, dtype=torch.int32, device=self.device)
+        self.tok_sums = torch.empty(max(n, 1) * 9, **f64)
         self.cder = abi.FateDerived(mean_base=self.mean_base.data_ptr(),
                                     demand=self.demand.data_ptr(),
                                     split_penalty=self.split_penalty.data_ptr(),
@@ -261,7 +263,9 @@ class DeviceBank:
                                     inst_qgroups=self.inst_qgroups.data_ptr(),
                                     tail_sum=self.tail_sum.data_ptr(),
                                     tail_static=self.tail_static.data_ptr(),
-                                    stage_rec=self.stage_rec.data_ptr())
+                                    stage_rec=self.stage_rec.data_ptr(),
+                                    tok_vals=self.tok_vals.data_ptr(),
+                                    tok_sums=self.tok_sums.data_ptr())
         s = stream or torch.cuda.current_stream(self.device)
         # op templates of the tail (v6 kernel): count per (stage, level), scan, fill
         nvl = n * self.levels

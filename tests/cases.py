@@ -180,4 +180,61 @@ def edge_case(seed: int = 7, horizon: int = 4, ablation=None, overrides=True):
     return Case(f"edge-h{horizon}", [inst], c, weights, states, items)
 
 
+def token_case(seed: int = 3, horizon: int = 3):
+    """Uniform speeds, no query prefix groups, one big prefix group whose
+    keep_cache stages have five distinct prompts, and prefix entries whose
+    token counts are those prompts, other counts, or under other models: every
+    kind of class the kernel's partial-hit tables (tok_vals/tok_sums) see --
+    tabulated, beyond the three tabulated values, untabulated counts, full
+    hits, misses -- next to shard bounds 1-3."""
+    rng = random.Random(seed)
+    cfg = default_config(6)
+    topo = cfg.topology
+    models = cfg.models
+    aliases = sorted(models)
+    roles = list(cfg.roles.values())
+    ids = [f"t{i:02d}" for i in range(24)]
+    levels = [ids[0:6], ids[6:12], ids[12:18], ids[18:24]]
+    edges = set()
+    for li in range(1, len(levels)):
+        for v in levels[li]:
+            ups = [u for u in levels[li - 1] if rng.random() < 0.5] or [levels[li - 1][0]]
+            edges.update((u, v) for u in ups)
+    prompts = [100, 200, 300, 400, 500]
+    stages = {}
+    for i, sid in enumerate(ids):
+        role = roles[i % len(roles)]
+        shard = 1 if not role.shard_eligible else [1, 2, 3][i % 3]
+        stages[sid] = Stage(id=sid, model=aliases[i % 2], eligible_devices=frozenset(topo.device_ids),
+                            shard_bound=shard, role=role,
+                            prompt_token_proxy=prompts[i % 5] + (0 if i % 7 else 100),
+                            output_token_proxy=rng.choice([128, 384]),
+                            shared_prefix_group="pg" if i % 6 else "other",
+                            keep_cache=bool(i % 2 == 0 or i % 5 == 3), cache_reuse=True)
+    dag = annotate_topology(WorkflowDag("tok", "tok", stages, frozenset(edges)))
+    queries = tuple(Query(f"q{i:03d}", 100 + rng.randrange(700), None) for i in range(16))
+    inst = WorkflowInstance(dag=dag, queries=queries, batch_size=16, prefix_groups={})
+    weights = replace(cfg.weights, horizon=horizon)
+    states = []
+    for s in range(5):
+        st = ExecutionState.initial(inst, topo.device_ids)
+        st.clock = 50.0 * s
+        r2 = random.Random(500 + s)
+        for sid in sorted(ids)[: 4 * s]:
+            st.parent_loc[sid] = ((r2.choice(topo.device_ids), tuple(q.query_id for q in queries)),)
+            st.completed.add(sid)
+        for d in topo.device_ids:
+            st.residency[d] = r2.choice(aliases)
+            st.device_free[d] = st.clock + r2.choice([-5.0, 0.0, 4.0])
+            store = st.prefix_store[d]
+            tok = r2.choice([100, 200, 300, 400, 500, 600, 250, 1000])
+            store["pg"] = PrefixEntry("pg", tok, r2.choice(aliases), sticky=r2.random() < 0.5)
+            if r2.random() < 0.5:
+                store["other"] = PrefixEntry("other", r2.choice([100, 300]), r2.choice(aliases))
+        states.append((0, st))
+    bank_tmp = pack.pack_bank([inst], models, topo)
+    items = [(j, bank_tmp.global_index(0, sid)) for j in range(len(states)) for sid in ids]
+    return Case(f"tok-h{horizon}", [inst], cfg, weights, states, items)
+
+
 ALL_ABLATIONS = ("no_future_planning", "no_locality", "no_same_model", "no_prefix", "no_shard")

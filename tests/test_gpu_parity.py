@@ -16,7 +16,7 @@ import oracle
 from paper_2605_07238_b200 import pack, runtime
 from paper_2605_07238_b200.wf.weights import AblationFlags
 
-from cases import ALL_ABLATIONS, bits, c4_case, c5_case, edge_case, small_case
+from cases import ALL_ABLATIONS, bits, c4_case, c5_case, edge_case, small_case, token_case
 
 pytestmark = pytest.mark.gpu
 
@@ -61,6 +61,13 @@ def test_lifted_scenarios():
 
 def test_prefix_suite_scenarios():
     assert_parity(small_case(prefix=True))
+
+
+@pytest.mark.parametrize("horizon", [0, 3])
+def test_partial_hit_token_classes(horizon):
+    """Tabulated partial-hit prefix classes (tok_vals / tok_sums) next to
+    untabulated ones, full hits and misses."""
+    assert_parity(token_case(horizon=horizon))
 
 
 def test_c5_frontier():

@@ -16,7 +16,7 @@ import pytest
 import oracle
 from paper_2605_07238_b200.wf.weights import AblationFlags
 
-from cases import ALL_ABLATIONS, bits, c5_case, edge_case, small_case
+from cases import ALL_ABLATIONS, bits, c5_case, edge_case, small_case, token_case
 
 pytestmark = pytest.mark.reference
 
@@ -103,3 +103,7 @@ def test_prefix_suite_scenarios(reference):
 
 def test_c5_frontier(reference):
     _check(reference, _with_objs(c5_case, n_inst=2))
+
+
+def test_partial_hit_token_case(reference):
+    _check(reference, _with_objs(token_case, horizon=3))
