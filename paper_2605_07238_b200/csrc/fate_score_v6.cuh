@@ -268,6 +268,27 @@ __device__ __forceinline__ void v6_apply(double (&aff)[DPL], double val, int k, 
     }
 }
 
+// state.cached_tokens (state.py:110-123) for the stage group, with the first
+// two entries loaded speculatively next to the entry count (one dependent load
+// level less on the critical path; entries past the count are never used)
+__device__ __forceinline__ int v6_cached_tokens(const int32_t* __restrict__ kap,
+                                                const int32_t* __restrict__ kn_p, int cap,
+                                                int group, int model) {
+    if (group == -1) return 0;
+    const int4* e = reinterpret_cast<const int4*>(kap);
+    const int n = __ldg(kn_p);
+    const int4 e0 = __ldg(e);
+    const int4 e1 = cap > 1 ? __ldg(e + 1) : e0;
+    if (n > 0 && e0.x == group) return (model != -1 && e0.z != model) ? 0 : e0.y;
+    if (n > 1 && e1.x == group) return (model != -1 && e1.z != model) ? 0 : e1.y;
+#pragma unroll 1
+    for (int k = 2; k < n; ++k) {
+        const int4 x = __ldg(e + k);
+        if (x.x == group) return (model != -1 && x.z != model) ? 0 : x.y;
+    }
+    return 0;
+}
+
 struct V6Item {
     int q0, nq, m, Pv;
     long long dev_row0;
@@ -418,7 +439,8 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         if (live[j]) {
             if (cache_reuse) {
                 const long long row = it.dev_row0 + dv[j];
-                const int c = cached_tokens(st.kappa + row * it.cap4, st.kappa_n[row], gv, m);
+                const int c = v6_cached_tokens(st.kappa + row * it.cap4, st.kappa_n + row,
+                                               st.kappa_cap, gv, m);
                 cs[j] = it.Pv - c > 0 ? it.Pv - c : 0;
             }
             s_key[dv[j]] = cs[j];
