@@ -290,6 +290,47 @@ typedef struct fate_selection {
 int fate_solve_frontier(const fate_frontier* p, double budget_s, int64_t max_options,
                         fate_selection* out);
 
+/* ---- device-resident execution-state mirror -----------
+ * One running workflow instance's scorer state kept in HBM and updated in
+ * place from the executor's transitions (reference state.py:130-272), plus
+ * the GPU ready set (model.py:306-319).  fate_mirror_state exposes the
+ * mirror as a one-scenario fate_state that fate_score reads directly -- no
+ * per-wave snapshot / pack / upload. */
+#define FATE_EV_COMMIT 0    /* commit_stage(stage, slots) */
+#define FATE_EV_START 1     /* on_task_start: stage, device, time = finish_time */
+#define FATE_EV_COMPLETE 2  /* on_task_complete: stage, device, time = finish,
+                               queries = event_queries[q0 .. q0+nq) */
+
+typedef struct fate_event {
+    int32_t kind;
+    int32_t stage;                  /* global stage index */
+    int32_t device;
+    int32_t slots;                  /* COMMIT: total slots of the stage */
+    double time;
+    int32_t q0;
+    int32_t nq;
+} fate_event;
+
+typedef struct fate_mirror fate_mirror;
+
+/* bank: the device bank holding the instance; q_group_host / q_tokens_host:
+ * per query of the instance its prefix group id (-1 None) and
+ * group_tokens(group, prompt) (state.py:79-85), HOST; empty_model: the model
+ * id the bank gives "" (entries seeded by model-less stages). */
+int fate_mirror_create(const fate_bank* bank, int32_t inst, int32_t kappa_cap,
+                       const int32_t* q_group_host, const int32_t* q_tokens_host,
+                       int32_t empty_model, void* stream, fate_mirror** out);
+int fate_mirror_destroy(fate_mirror* m);
+/* Apply events (HOST arrays, in executor order) on `stream`. */
+int fate_mirror_apply(fate_mirror* m, const fate_event* events, int32_t n_events,
+                      const int32_t* event_queries, int32_t n_event_queries, void* stream);
+/* The mirror as a one-scenario fate_state (device pointers; scenario 0). */
+int fate_mirror_state(const fate_mirror* m, fate_state* out);
+/* Ready stages (global indices, ascending) into out_dev (device, >= stage
+ * count of the instance); *n_out (host) after a stream synchronize.  Reports
+ * errors recorded by earlier applies (kappa overflow, bad event). */
+int fate_mirror_ready(fate_mirror* m, int32_t* out_dev, int32_t* n_out, void* stream);
+
 /* Device: count kernel launches issued by this library since load (for the
  * benchmark's gpu_launches evidence). */
 int64_t fate_launch_count(void);

@@ -21,7 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfate.so")
 SOURCES = [os.path.join(CSRC, "fate_kernels.cu"), os.path.join(CSRC, "fate_host.cpp"),
            os.path.join(CSRC, "fate_synth.cpp"), os.path.join(CSRC, "fate_pipeline.cpp"),
-           os.path.join(CSRC, "fate_solver.cpp")]
+           os.path.join(CSRC, "fate_solver.cpp"), os.path.join(CSRC, "fate_mirror.cu")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-ffp-contract=off", "-I", INCLUDE]

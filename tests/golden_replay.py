@@ -151,10 +151,10 @@ def record_mismatches(rec, want: dict) -> list:
 
 
 def replay(run_meta: dict, arrays: dict, instance, config, scorer, seed: int = 0,
-           solver: str = "python"):
+           solver: str = "python", observer=None):
     chk = CheckingScorer(scorer, run_meta, arrays)
     policy = FateGpuPolicy(scorer=chk, solver=solver)
-    rec = run(policy, instance, config, seed=seed)
+    rec = run(policy, instance, config, seed=seed, observer=observer)
     problems = list(chk.mismatches)
     if chk.i != len(run_meta["waves"]):
         problems.append(f"{chk.i} waves != golden {len(run_meta['waves'])}")

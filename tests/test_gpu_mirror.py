@@ -1,0 +1,72 @@
+"""Device-resident state mirror + GPU ready set (csrc/fate_mirror.cu,
+SURVEY §8(f) row 2): full FATE runs scored from the mirror reproduce the
+captured reference runs wave by wave (Psi, S, completion bits) and in their
+RunRecords; the GPU ready set equals the executor's frontier at every wave;
+the mirror's arrays equal pack_states(snapshot)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2605_07238_b200 import pack
+from paper_2605_07238_b200.mirror import MirrorScorer
+
+import golden_replay as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_mirror_replays_golden_runs(name):
+    runs, arrs = G.load(name)
+    bad = []
+    n_waves = 0
+    for r in runs:
+        if name == "c1":
+            inst, cfg = G.c1_setup(r["variant"])
+        elif name == "c2":
+            inst, cfg = G.c2_setup(r["key"])
+        else:
+            inst, cfg = G.c3_setup(r["ratio"], r["batch"], r["shape"])
+        scorer = MirrorScorer(check_ready=True)
+        _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, observer=scorer)
+        n_waves += scorer.ready_checks
+        if problems:
+            bad.append(problems[:3])
+    assert not bad, bad
+    assert n_waves > 0
+
+
+def test_mirror_arrays_equal_packed_snapshot():
+    """At every wave of a config-1 run, the mirror's residency, device_free,
+    prefix entries (group, tokens, model), loc, clock and done level equal
+    pack_states of the executor's snapshot."""
+    runs, arrs = G.load("c1")
+    r = runs[0]
+    inst, cfg = G.c1_setup(r["variant"])
+    checks = []
+
+    class Spy(MirrorScorer):
+        def score_wave(self, frontier, state, cost_model, dag=None):
+            ws = super().score_wave(frontier, state, cost_model, dag)
+            got = self.mirror.download()
+            packed = self.mirror.dbank.packed
+            want = pack.pack_states(packed, [(0, state)], kappa_cap=self.kappa_cap).arrays
+            D = packed.scalars["n_devices"]
+            for k in ("residency", "dev_free", "kappa_n", "scen_clock", "scen_done_level"):
+                assert np.array_equal(np.asarray(got[k]), np.asarray(want[k])), k
+            n = len(self.mirror.stage_ids)
+            assert np.array_equal(got["loc"][:n], np.asarray(want["loc"])[:n])
+            gk = got["kappa"].reshape(D, self.kappa_cap, 4)
+            wk = np.asarray(want["kappa"]).reshape(D, self.kappa_cap, 4)
+            for d in range(D):
+                m = int(want["kappa_n"][d])
+                assert np.array_equal(gk[d, :m, :3], wk[d, :m, :3]), d
+            checks.append(1)
+            return ws
+
+    scorer = Spy(check_ready=True)
+    _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, observer=scorer)
+    assert not problems, problems[:3]
+    assert len(checks) == len(r["waves"])

@@ -1,0 +1,60 @@
+"""Per-wave scorer cost of a long FATE run: snapshot -> pack -> upload
+(GpuScorer) vs the device-resident mirror (MirrorScorer, events applied on the
+GPU).  Prints one JSON line per scorer.  Native solver at budget 0 keeps the
+run itself fast; the scorer time is what differs."""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2605_07238_b200.mirror import MirrorScorer  # noqa: E402
+from paper_2605_07238_b200.planner import FateGpuPolicy, GpuScorer  # noqa: E402
+from paper_2605_07238_b200.wf import workloads as W  # noqa: E402
+from paper_2605_07238_b200.wf.simulate import run  # noqa: E402
+from paper_2605_07238_b200.wf.weights import default_config  # noqa: E402
+from dataclasses import replace  # noqa: E402
+
+
+class Timed:
+    def __init__(self, inner):
+        self.inner = inner
+        self.t = 0.0
+        self.waves = 0
+
+    def score_wave(self, *a, **k):
+        t0 = time.perf_counter()
+        out = self.inner.score_wave(*a, **k)
+        self.t += time.perf_counter() - t0
+        self.waves += 1
+        return out
+
+
+def main():
+    depth, width = (int(x) for x in (sys.argv[1:3] if len(sys.argv) > 2 else (40, 50)))
+    cfg = default_config(16)
+    cfg = cfg.with_weights(replace(cfg.weights, horizon=3))
+    dag = W.synth_generate(W.SuiteSpec(kind="synthetic", depth=depth, width=width, density=0.05,
+                                       seed=7, batch_size=16), cfg)
+    inst = W.make_instance(dag, 16, 7)
+    recs = {}
+    for name in ("snapshot+pack", "mirror"):
+        inner = GpuScorer() if name == "snapshot+pack" else MirrorScorer()
+        sc = Timed(inner)
+        pol = FateGpuPolicy(scorer=sc, solver="native", solver_budget_s=0.0)
+        t0 = time.perf_counter()
+        rec = run(pol, inst, cfg, observer=inner if name == "mirror" else None)
+        wall = time.perf_counter() - t0
+        recs[name] = rec
+        print(json.dumps({"scorer": name, "stages": len(dag.stages), "waves": sc.waves,
+                          "score_ms_per_wave": 1e3 * sc.t / max(sc.waves, 1),
+                          "run_s": wall, "makespan": rec.makespan}), flush=True)
+    a, b = recs["snapshot+pack"], recs["mirror"]
+    print(json.dumps({"identical_record": (a.makespan, a.query_completion, a.workflow_tasks) ==
+                      (b.makespan, b.query_completion, b.workflow_tasks)}))
+
+
+if __name__ == "__main__":
+    main()
