@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -225,17 +226,18 @@ __global__ void fate_prepare_demand_kernel(fate_bank b, fate_windows win, fate_d
 #include "fate_score_v5.cuh"
 #include "fate_score_v6.cuh"
 
-template <int DPL, bool OVR, int MINB>
+template <int DPL, bool OVR, bool SL, int MINB>
 int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                  const fate_derived* der, const fate_state* st, const fate_work* work,
                  const fate_out* out, cudaStream_t s) {
     if (!der->stage_rec || (win->levels > 0 && (!der->tmpl_ptr || !der->tmpl)))
         return fail(FATE_ENOTREADY, "v6 kernel needs stage records and op templates");
-    const V6Layout lay = v6_layout(bank->n_devices, bank->max_queries, win->max_level_ops);
+    const V6Layout lay = SL ? v6_layout_static(win->max_level_ops)
+                            : v6_layout(bank->n_devices, bank->max_queries, win->max_level_ops);
     const size_t smem = (size_t)lay.item_bytes * 4;
     if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v6 shared-memory footprint too large");
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fate_score_v6_kernel<DPL, OVR, MINB>,
+        cudaFuncSetAttribute(fate_score_v6_kernel<DPL, OVR, SL, MINB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // persistent grid: every resident CTA slot once (capped by the item count)
     static thread_local size_t occ_smem = ~size_t(0);
@@ -243,11 +245,11 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     static thread_local const void* occ_fn = nullptr;
     int dev = 0;
     cudaGetDevice(&dev);
-    const void* fn = (const void*)fate_score_v6_kernel<DPL, OVR, MINB>;
+    const void* fn = (const void*)fate_score_v6_kernel<DPL, OVR, SL, MINB>;
     if (occ_smem != smem || occ_dev != dev || occ_fn != fn) {
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fate_score_v6_kernel<DPL, OVR, MINB>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fate_score_v6_kernel<DPL, OVR, SL, MINB>,
                                                       128, smem);
         o = std::max(1, sms * std::max(1, per));
         occ_smem = smem;
@@ -268,7 +270,7 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     const unsigned blocks = (unsigned)std::min<long long>(o, want);
     static std::atomic<int> slot{0};
     const int qs = slot.fetch_add(1) % V6_QSLOTS;
-    fate_score_v6_kernel<DPL, OVR, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
+    fate_score_v6_kernel<DPL, OVR, SL, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
                                                                     *work, *out, lay, qs, fetch);
     return 0;
 }
@@ -312,26 +314,41 @@ int launch_v5(const fate_bank* bank, const fate_weights* w, const fate_windows* 
     }
 }
 
-template <int DPL>
-int launch_v6(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
-              const fate_derived* der, const fate_state* st, const fate_work* work,
-              const fate_out* out, cudaStream_t s) {
+template <int DPL, bool SL>
+int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+                 const fate_derived* der, const fate_state* st, const fate_work* work,
+                 const fate_out* out, cudaStream_t s) {
     const bool ovr = bank->has_overrides != 0;
     const char* e = getenv("FATE_MINB");
     switch (e ? atoi(e) : (DPL == 1 ? 8 : 7)) {
         case 1:
-            return ovr ? launch_v6_mb<DPL, true, 1>(bank, w, win, der, st, work, out, s)
-                       : launch_v6_mb<DPL, false, 1>(bank, w, win, der, st, work, out, s);
-        case 7:
-            return ovr ? launch_v6_mb<DPL, true, 7>(bank, w, win, der, st, work, out, s)
-                       : launch_v6_mb<DPL, false, 7>(bank, w, win, der, st, work, out, s);
+            return ovr ? launch_v6_mb<DPL, true, SL, 1>(bank, w, win, der, st, work, out, s)
+                       : launch_v6_mb<DPL, false, SL, 1>(bank, w, win, der, st, work, out, s);
         case 6:
-            return ovr ? launch_v6_mb<DPL, true, 6>(bank, w, win, der, st, work, out, s)
-                       : launch_v6_mb<DPL, false, 6>(bank, w, win, der, st, work, out, s);
+            return ovr ? launch_v6_mb<DPL, true, SL, 6>(bank, w, win, der, st, work, out, s)
+                       : launch_v6_mb<DPL, false, SL, 6>(bank, w, win, der, st, work, out, s);
+        case 7:
+            return ovr ? launch_v6_mb<DPL, true, SL, 7>(bank, w, win, der, st, work, out, s)
+                       : launch_v6_mb<DPL, false, SL, 7>(bank, w, win, der, st, work, out, s);
         default:
-            return ovr ? launch_v6_mb<DPL, true, 8>(bank, w, win, der, st, work, out, s)
-                       : launch_v6_mb<DPL, false, 8>(bank, w, win, der, st, work, out, s);
+            return ovr ? launch_v6_mb<DPL, true, SL, 8>(bank, w, win, der, st, work, out, s)
+                       : launch_v6_mb<DPL, false, SL, 8>(bank, w, win, der, st, work, out, s);
     }
+}
+
+// Static shared-memory layout for D > 32 when the query batch fits V6S_B
+// (measured: C4 -4.5 %); for D <= 32 the larger static slice costs L1 capacity
+// the gathers need (C5 +4 %), so the runtime layout stays.  FATE_V6_DYNLAYOUT /
+// FATE_V6_STATICLAYOUT force one (A/B only).
+template <int DPL>
+int launch_v6(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+              const fate_derived* der, const fate_state* st, const fate_work* work,
+              const fate_out* out, cudaStream_t s) {
+    static const bool dyn = getenv("FATE_V6_DYNLAYOUT") != nullptr;
+    static const bool stat = getenv("FATE_V6_STATICLAYOUT") != nullptr;
+    if (!dyn && (DPL == 2 || stat) && bank->max_queries <= V6S_B)
+        return launch_v6_sl<DPL, true>(bank, w, win, der, st, work, out, s);
+    return launch_v6_sl<DPL, false>(bank, w, win, der, st, work, out, s);
 }
 
 // Kernel generation: v6 (production) needs the stage records and op templates

@@ -70,6 +70,40 @@ struct V6Layout {
     int rows, shard, aware, sw, tr, opval, opkey, key, cslot, rowdev;
 };
 
+// Static per-warp layout for the common shapes (query batch <= V6S_B, any
+// D <= 64): every field at a compile-time offset from the warp's slice base,
+// so the many shared-memory accesses use immediate offsets and the compiler's
+// rematerialisation under the register budget is a base re-derivation, not a
+// reload of runtime offsets.  The op buffers (size set by the windows) follow.
+constexpr int V6S_B = 32;
+struct __align__(16) V6SmemS {
+    double rows[V6_RCAP * V6S_B];
+    double shard[V6_SLOTS * 2 * V6_KT];
+    double aware[(V6_SLOTS + 1) & ~1];
+    double sw[FATE_MAX_DEVICES];
+    double tr[FATE_MAX_DEVICES];
+    int key[FATE_MAX_DEVICES];
+    int cslot[FATE_MAX_DEVICES];
+    int rowdev[V6_RCAP];
+};
+
+inline V6Layout v6_layout_static(int ops_cap) {
+    V6Layout L{};
+    const int ops4 = ((ops_cap > 0 ? ops_cap : 1) + 3) & ~3;
+    L.rows = (int)offsetof(V6SmemS, rows);
+    L.shard = (int)offsetof(V6SmemS, shard);
+    L.aware = (int)offsetof(V6SmemS, aware);
+    L.sw = (int)offsetof(V6SmemS, sw);
+    L.tr = (int)offsetof(V6SmemS, tr);
+    L.key = (int)offsetof(V6SmemS, key);
+    L.cslot = (int)offsetof(V6SmemS, cslot);
+    L.rowdev = (int)offsetof(V6SmemS, rowdev);
+    L.opval = (int)((sizeof(V6SmemS) + 15) & ~size_t(15));
+    L.opkey = L.opval + 8 * ops4;
+    L.item_bytes = (L.opkey + 4 * ops4 + 15) & ~15;
+    return L;
+}
+
 inline V6Layout v6_layout(int D, int Bmax, int ops_cap) {
     V6Layout L{};
     int o = 0;
@@ -315,27 +349,30 @@ __device__ __forceinline__ double v6_qc(const fate_bank& b, const fate_state& st
 // scoring kernel
 // ---------------------------------------------------------------------------
 
-// One item (scenario, stage v) by one warp; sb = the warp's shared-memory slice.
-template <int DPL, bool OVR>
+// One item (scenario, stage v) by one warp; sb = the warp's shared-memory slice
+// (static layout V6SmemS when SL, else the runtime layout `lay`).
+template <int DPL, bool OVR, bool SL>
 __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& w,
                                         const fate_windows& win, const fate_derived& der,
                                         const fate_state& st, const fate_work& work,
                                         const fate_out& out, const V6Layout& lay,
                                         const long long item, unsigned char* sb) {
     const int t = threadIdx.x & 31;
-    double* const s_rows = reinterpret_cast<double*>(sb + lay.rows);
-    double* const s_shard = reinterpret_cast<double*>(sb + lay.shard);
-    double* const s_aware = reinterpret_cast<double*>(sb + lay.aware);
-    double* const s_sw = reinterpret_cast<double*>(sb + lay.sw);
-    double* const s_tr = reinterpret_cast<double*>(sb + lay.tr);
+    V6SmemS* const ss = reinterpret_cast<V6SmemS*>(sb);
+    double* const s_rows = SL ? ss->rows : reinterpret_cast<double*>(sb + lay.rows);
+    double* const s_shard = SL ? ss->shard : reinterpret_cast<double*>(sb + lay.shard);
+    double* const s_aware = SL ? ss->aware : reinterpret_cast<double*>(sb + lay.aware);
+    double* const s_sw = SL ? ss->sw : reinterpret_cast<double*>(sb + lay.sw);
+    double* const s_tr = SL ? ss->tr : reinterpret_cast<double*>(sb + lay.tr);
     double* const s_opval = reinterpret_cast<double*>(sb + lay.opval);
     int* const s_opkey = reinterpret_cast<int*>(sb + lay.opkey);
-    int* const s_key = reinterpret_cast<int*>(sb + lay.key);
-    int* const s_cslot = reinterpret_cast<int*>(sb + lay.cslot);
-    int* const s_rowdev = reinterpret_cast<int*>(sb + lay.rowdev);
+    int* const s_key = SL ? ss->key : reinterpret_cast<int*>(sb + lay.key);
+    int* const s_cslot = SL ? ss->cslot : reinterpret_cast<int*>(sb + lay.cslot);
+    int* const s_rowdev = SL ? ss->rowdev : reinterpret_cast<int*>(sb + lay.rowdev);
 
     const unsigned FULL = 0xffffffffu;
-    const int D = b.n_devices, Bmax = b.max_queries, LV = win.levels;
+    const int D = b.n_devices, LV = win.levels;
+    const int Bmax = SL ? V6S_B : b.max_queries;  // row stride of s_rows
     const bool no_loc = w.ablation & FATE_NO_LOCALITY;
     const bool no_shard = w.ablation & FATE_NO_SHARD;
     const int H = w.eff_horizon;
@@ -906,7 +943,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 constexpr int V6_QSLOTS = 128;
 __device__ unsigned int g_v6_queue[2 * V6_QSLOTS];  // per slot: next ticket, warps done
 
-template <int DPL, bool OVR, int MINB>
+template <int DPL, bool OVR, bool SL, int MINB>
 __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, fate_weights w,
                                                                   fate_windows win,
                                                                   fate_derived der, fate_state st,
@@ -938,7 +975,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
         const long long i1 = (long long)i + take < n ? (long long)i + take : n;
 #pragma unroll 1
         for (long long it = i; it < i1; ++it) {
-            v6_item<DPL, OVR>(b, w, win, der, st, work, out, lay, it, sb);
+            v6_item<DPL, OVR, SL>(b, w, win, der, st, work, out, lay, it, sb);
             __syncwarp();  // the slice is reused by the next item
         }
     }
