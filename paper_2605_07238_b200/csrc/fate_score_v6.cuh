@@ -959,12 +959,12 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
     // 1/(4 * warps) of what the warp last saw remaining (at least one), so
     // early tickets are large (few atomics) and late ones single items (tail
     // balance)
-    const long long n_warps = (long long)gridDim.x * (blockDim.x >> 5);
+    const float inv_share = 0.25f / (float)(gridDim.x * (blockDim.x >> 5));
     long long seen = 0;
     for (;;) {
         long long take = fetch;
-        if (fetch == 0) {
-            take = (n - seen) / (4 * n_warps);
+        if (fetch == 0) {  // heuristic size: a float estimate is enough
+            take = (long long)((float)(n - seen) * inv_share);
             take = take < 1 ? 1 : (take > 16 ? 16 : take);
         }
         unsigned int i = 0;
