@@ -186,10 +186,15 @@ class MirrorScorer(GpuScorer):
     running instance instead of packing the per-wave snapshot.  Pass it both as
     the policy's scorer and as ``simulate.run(..., observer=scorer)``."""
 
-    def __init__(self, device=None, kappa_cap: int = 16, check_ready: bool = False):
+    def __init__(self, device=None, kappa_cap: int = 16, check_ready: bool = False,
+                 gpu_frontier: bool = False):
+        """``check_ready``: assert the GPU ready set equals the executor's
+        frontier every wave.  ``gpu_frontier``: the executor takes each wave's
+        frontier from the GPU ready set (``frontier()``)."""
         super().__init__(device=device)
         self.kappa_cap = kappa_cap
         self.check_ready = check_ready
+        self.provides_frontier = gpu_frontier
         self.mirror: DeviceMirror | None = None
         self._instance = None
         self.ready_checks = 0
@@ -202,6 +207,10 @@ class MirrorScorer(GpuScorer):
         self.mirror = DeviceMirror(dbank, 0, self.kappa_cap)
         self.mirror.attach(state)
         self._instance = state.instance
+
+    def frontier(self) -> list:
+        """The next wave's frontier: the GPU ready set (model.py:306-319)."""
+        return self.mirror.ready()
 
     def score_wave(self, frontier, state, cost_model, dag=None) -> WaveScores:
         if self.mirror is None or state.instance is not self._instance:

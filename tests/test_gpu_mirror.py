@@ -70,3 +70,21 @@ def test_mirror_arrays_equal_packed_snapshot():
     _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, observer=scorer)
     assert not problems, problems[:3]
     assert len(checks) == len(r["waves"])
+
+
+def test_executor_on_gpu_frontier_matches_golden_records():
+    """The executor taking every wave's frontier from the GPU ready set
+    (gpu_frontier) reproduces the captured config-1 and config-3 runs."""
+    bad = []
+    for name in ("c1", "c3"):
+        runs, arrs = G.load(name)
+        for r in runs:
+            if name == "c1":
+                inst, cfg = G.c1_setup(r["variant"])
+            else:
+                inst, cfg = G.c3_setup(r["ratio"], r["batch"], r["shape"])
+            scorer = MirrorScorer(gpu_frontier=True)
+            _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, observer=scorer)
+            if problems:
+                bad.append((name, problems[:3]))
+    assert not bad, bad

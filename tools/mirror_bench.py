@@ -40,20 +40,22 @@ def main():
                                        seed=7, batch_size=16), cfg)
     inst = W.make_instance(dag, 16, 7)
     recs = {}
-    for name in ("snapshot+pack", "mirror"):
-        inner = GpuScorer() if name == "snapshot+pack" else MirrorScorer()
+    for name in ("snapshot+pack", "mirror", "mirror+gpu_frontier"):
+        inner = (GpuScorer() if name == "snapshot+pack"
+                 else MirrorScorer(gpu_frontier=name.endswith("frontier")))
         sc = Timed(inner)
         pol = FateGpuPolicy(scorer=sc, solver="native", solver_budget_s=0.0)
         t0 = time.perf_counter()
-        rec = run(pol, inst, cfg, observer=inner if name == "mirror" else None)
+        rec = run(pol, inst, cfg, observer=None if name == "snapshot+pack" else inner)
         wall = time.perf_counter() - t0
         recs[name] = rec
         print(json.dumps({"scorer": name, "stages": len(dag.stages), "waves": sc.waves,
                           "score_ms_per_wave": 1e3 * sc.t / max(sc.waves, 1),
                           "run_s": wall, "makespan": rec.makespan}), flush=True)
-    a, b = recs["snapshot+pack"], recs["mirror"]
-    print(json.dumps({"identical_record": (a.makespan, a.query_completion, a.workflow_tasks) ==
-                      (b.makespan, b.query_completion, b.workflow_tasks)}))
+    a = recs["snapshot+pack"]
+    print(json.dumps({"identical_record": all(
+        (a.makespan, a.query_completion, a.workflow_tasks) ==
+        (b.makespan, b.query_completion, b.workflow_tasks) for b in recs.values())}))
 
 
 if __name__ == "__main__":
