@@ -88,3 +88,36 @@ def test_executor_on_gpu_frontier_matches_golden_records():
             if problems:
                 bad.append((name, problems[:3]))
     assert not bad, bad
+
+
+def test_mirror_reports_prefix_overflow_and_bad_events():
+    import ctypes as C
+
+    from paper_2605_07238_b200 import mirror as M
+    from paper_2605_07238_b200.runtime import DeviceBank
+
+    runs, arrs = G.load("c1")
+    inst, cfg = G.c1_setup(runs[0]["variant"])
+    dbank = DeviceBank(pack.pack_bank([inst], cfg.models, cfg.topology), cfg.weights)
+    m = M.DeviceMirror(dbank, 0, kappa_cap=1)
+    groups = [g for g, i in sorted(dbank.packed.group_index.items(), key=lambda kv: kv[1])]
+    # two stages of different groups completing on device 0 overflow kappa_cap = 1
+    sids = [s for s in m.stage_ids if inst.dag.stages[s].keep_cache
+            and inst.dag.stages[s].shared_prefix_group is not None]
+    by_group = {}
+    for s in sids:
+        by_group.setdefault(inst.dag.stages[s].shared_prefix_group, s)
+    two = list(by_group.values())[:2]
+    assert len(two) == 2 and groups
+    for sid in two:
+        m.pending.append((M.EV_COMMIT, m._g(sid), -1, 1, 0.0, 0, 0))
+        m.pending.append((M.EV_START, m._g(sid), 0, 0, 1.0, 0, 0))
+        m.pending.append((M.EV_COMPLETE, m._g(sid), 0, 0, 1.0, 0, 0))
+    with pytest.raises(ValueError):  # FATE_ETOOBIG -> status < 0
+        m.ready()
+    m.close()
+    m = M.DeviceMirror(dbank, 0, kappa_cap=4)
+    m.pending.append((M.EV_START, m._g(two[0]), 999, 0, 1.0, 0, 0))  # device out of range
+    with pytest.raises(ValueError):
+        m.ready()
+    m.close()

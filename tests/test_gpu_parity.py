@@ -163,3 +163,27 @@ def test_host_pipeline_skips_scenarios_without_items():
     assert np.array_equal(bits(got.numpy()[: sub.n_psi]), bits(want))
     full = sum(v.nbytes for v in case.states.arrays.values())
     assert pipe.h2d_bytes < full
+
+
+def test_host_pipeline_rejects_contract_violations():
+    """Unsorted items / out-of-range scenarios fail with ValueError (status < 0)
+    before any copy is enqueued."""
+    import ctypes as C
+
+    from paper_2605_07238_b200 import abi
+
+    case = c5_case(n_inst=2)
+    dbank = runtime.DeviceBank(case.bank, case.weights)
+    pipe = runtime.HostPipeline(dbank, case.states, case.work, n_chunks=2)
+    items = pipe.h_items.numpy().view(pack.ITEM_DTYPE)
+    saved = items.copy()
+    items["scen"][0], items["scen"][-1] = items["scen"][-1], items["scen"][0]
+    with pytest.raises(ValueError):
+        pipe.run()
+    items[:] = saved
+    items["scen"][0] = case.states.n_scenarios + 5
+    with pytest.raises(ValueError):
+        pipe.run()
+    items[:] = saved
+    pipe.run()  # valid again
+    pipe.close()

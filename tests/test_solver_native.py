@@ -134,3 +134,11 @@ def test_native_solver_replays_full_fate_runs(name):
         if problems:
             bad.append(problems[:3])
     assert not bad, bad
+
+
+def test_native_option_cap():
+    S = _native()
+    rng = random.Random(9)
+    prob = _problem(rng, 4, 6, max_bound=3)
+    with pytest.raises(ValueError):
+        S.solve_frontier(prob, budget_s=0.0, max_options=5)
