@@ -895,6 +895,28 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     }
 
     // ---- P4: per-device assembly ----------------------------------------------------------------
+    // Shard bound R = 2 with every class tabulated (one device slot per lane):
+    // a device's second shard always goes to the first idle device other than
+    // itself, so each device's shard-1 total sw + tr + shard sum is computed
+    // once and the two candidates (first / second idle device) are shuffled --
+    // the values and the max are _parallel_benefit's (costs.py:181-201) as in
+    // the general loop below.
+    bool fast2 = false;
+    double t1_e1 = 0.0, t1_e2 = 0.0;
+    int e1 = -1, e2 = -1;
+    if (DPL == 1 && R == 2 && !no_shard && kb == 2) {
+        const int sl = ok[0] ? s_cslot[dv[0]] : 0;
+        fast2 = __all_sync(FULL, sl >= 0);
+        if (fast2) {
+            const double t1self =
+                ok[0] ? s_sw[dv[0]] + s_tr[dv[0]] + s_shard[(sl * 2 + 0) * V6_KT + 1] : 0.0;
+            e1 = idle_m ? __ffsll((long long)idle_m) - 1 : 0;
+            const unsigned long long r2 = idle_m & (idle_m - 1ull);
+            e2 = r2 ? __ffsll((long long)r2) - 1 : 0;
+            t1_e1 = __shfl_sync(FULL, t1self, e1 & 31);
+            t1_e2 = __shfl_sync(FULL, t1self, e2 & 31);
+        }
+    }
     double* psi = out.psi + work.psi_off[item];
     const double split = no_loc ? 0.0 : (bound > 1 ? c2.y : 0.0);
     const bool no_pre = w.ablation & FATE_NO_PREFIX;
@@ -957,7 +979,14 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             const bool self_idle = (idle_m >> d) & 1ull;
             const int others = n_idle - (self_idle ? 1 : 0);
             const int k = R < 1 + others ? R : 1 + others;
-            if (k > 1) {
+            if (k > 1 && fast2) {
+                const int slot = s_cslot[d];
+                const double tot0 = s_sw[d] + s_tr[d] + s_shard[(slot * 2 + 0) * V6_KT + 0];
+                const double tot1 = d == e1 ? t1_e2 : t1_e1;
+                const double worst = tot1 > tot0 ? tot1 : tot0;
+                const double overhead = w.shard_overhead_frac * here_j * (double)(k - 1);
+                parallel = py_max0(full_total - worst - overhead);
+            } else if (k > 1) {
                 const int kslot = (k == kb && kb_ok) ? 0 : 1;
                 const bool tab = kslot == 0 || (k == ki && ki_ok);
                 unsigned long long rest = idle_m & ~(1ull << d);
