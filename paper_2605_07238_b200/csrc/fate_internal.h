@@ -15,6 +15,13 @@ int fate_internal_fail(int code, const std::string& msg);
 long long fate_internal_launches();
 void fate_internal_count_launches(long long n);
 
+// v6 ticket-queue slots: reserve one for a pipeline compute stream (-1 when
+// none is left), release it, and select the slot of this thread's next
+// scoring launch (-1 = the rotating direct-launch slots).
+int fate_internal_reserve_queue_slot();
+void fate_internal_release_queue_slot(int slot);
+void fate_internal_set_queue_slot(int slot);
+
 // Scatter wire-format scenario records [s0, s1) and items [i0, i1) (device
 // copies of fate_host_batch) into the fate_state / fate_work SoA of dst.
 // Wire loc rows [l0, l1) (int8) are widened into dst->loc.

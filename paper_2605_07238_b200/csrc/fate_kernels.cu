@@ -38,6 +38,9 @@
 namespace {
 
 thread_local std::string g_last_error;
+// queue slot for the next v6 launch of this thread (-1: rotate over the
+// direct-launch slots); set by the host pipeline around its scoring launches
+thread_local int g_queue_slot_override = -1;
 std::atomic<long long> g_launches{0};
 
 int fail(int code, const std::string& msg) {
@@ -269,7 +272,8 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     const long long want = (work->n_items + 3) / 4;
     const unsigned blocks = (unsigned)std::min<long long>(o, want);
     static std::atomic<int> slot{0};
-    const int qs = slot.fetch_add(1) % V6_QSLOTS;
+    const int qs = g_queue_slot_override >= 0 ? g_queue_slot_override
+                                              : slot.fetch_add(1) % V6_QDIRECT;
     fate_score_v6_kernel<DPL, OVR, SL, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
                                                                     *work, *out, lay, qs, fetch);
     return 0;
@@ -437,6 +441,26 @@ __global__ void fate_unpack_kernel(const unsigned char* __restrict__ rec, size_t
 int fate_internal_fail(int code, const std::string& msg) { return fail(code, msg); }
 
 long long fate_internal_launches() { return g_launches.load(); }
+
+namespace {
+std::atomic<unsigned long long> g_queue_used[(V6_QSLOTS - V6_QDIRECT + 63) / 64];
+}
+
+int fate_internal_reserve_queue_slot() {
+    for (int k = 0; k < V6_QSLOTS - V6_QDIRECT; ++k) {
+        const unsigned long long bit = 1ull << (k & 63);
+        if (!(g_queue_used[k / 64].fetch_or(bit) & bit)) return V6_QDIRECT + k;
+    }
+    return -1;  // all reserved: the caller's launches rotate like direct ones
+}
+
+void fate_internal_release_queue_slot(int slot) {
+    if (slot < V6_QDIRECT || slot >= V6_QSLOTS) return;
+    const int k = slot - V6_QDIRECT;
+    g_queue_used[k / 64].fetch_and(~(1ull << (k & 63)));
+}
+
+void fate_internal_set_queue_slot(int slot) { g_queue_slot_override = slot; }
 
 void fate_internal_count_launches(long long n) { g_launches += n; }
 

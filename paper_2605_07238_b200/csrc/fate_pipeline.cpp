@@ -41,6 +41,7 @@ struct fate_pipeline {
     std::vector<cudaEvent_t> in_ready;  // per chunk: its H2D copies landed
     std::vector<cudaEvent_t> scored;    // per chunk: its scoring launch finished
     cudaEvent_t start = nullptr;
+    std::vector<int> qslots;  // reserved ticket-queue slot per compute stream
     // captured graph of the last fate_pipeline_capture (replayed as a whole)
     cudaStream_t cap = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -106,6 +107,7 @@ int fate_pipeline_create(int device, int n_chunks, int n_streams, fate_pipeline*
             return cuda_fail(e, "fate_pipeline_create");
         }
     }
+    for (int i = 0; i < n_streams; ++i) p->qslots.push_back(fate_internal_reserve_queue_slot());
     p->in_ready.resize(n_chunks);
     p->scored.resize(n_chunks);
     for (int i = 0; i < n_chunks; ++i) {
@@ -139,6 +141,7 @@ int fate_pipeline_destroy(fate_pipeline* p) {
             if (ev) cudaEventDestroy(ev);
     if (p->start) cudaEventDestroy(p->start);
     if (p->exec) cudaGraphExecDestroy(p->exec);
+    for (int q : p->qslots) fate_internal_release_queue_slot(q);
     if (p->cap) cudaStreamDestroy(p->cap);
     cudaSetDevice(prev);
     delete p;
@@ -339,7 +342,10 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
         if (co.sched) co.sched += (size_t)k.i0 * D;
         if (co.completion) co.completion += (size_t)k.i0 * D;
         mark(s);
-        if ((rc = fate_score(bank, w, win, der, &dst, &cw, &co, s))) return rc;
+        fate_internal_set_queue_slot(p->qslots[c % p->qslots.size()]);
+        rc = fate_score(bank, w, win, der, &dst, &cw, &co, s);
+        fate_internal_set_queue_slot(-1);
+        if (rc) return rc;
         mark(s);
         if ((e = cudaEventRecord(p->scored[c], s)) != cudaSuccess)
             return cuda_fail(e, "fate_pipeline_score: score event");

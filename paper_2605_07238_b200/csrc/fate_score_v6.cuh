@@ -1061,9 +1061,13 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 // next one instead of holding a CTA slot idle (item costs vary several-fold
 // with the number of walked horizon levels, and consecutive items -- stages
 // of one scenario in index order -- have correlated costs).  Each launch uses
-// its own counter slot (host-side ring), and the last warp of a launch resets
-// the slot to zero, so a captured graph replays without a reset node.
-constexpr int V6_QSLOTS = 128;
+// its own counter slot and the last warp of a launch resets the slot to zero,
+// so a captured graph replays without a reset node.  Slots [0, V6_QDIRECT)
+// rotate over direct fate_score calls; the rest are reserved per host
+// pipeline compute stream (fate_internal_reserve_queue_slot), so a captured
+// pipeline graph never shares a counter with a concurrent direct launch.
+constexpr int V6_QSLOTS = 256;
+constexpr int V6_QDIRECT = 128;
 __device__ unsigned int g_v6_queue[2 * V6_QSLOTS];  // per slot: next ticket, warps done
 
 template <int DPL, bool OVR, bool SL, int MINB>
