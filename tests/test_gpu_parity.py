@@ -187,3 +187,32 @@ def test_host_pipeline_rejects_contract_violations():
     items[:] = saved
     pipe.run()  # valid again
     pipe.close()
+
+
+def test_concurrent_launches_on_streams_and_graph_replay():
+    """Scoring launches in flight on several streams at once, next to a
+    captured host pipeline, each keep their own work-queue counter: every
+    result equals the oracle."""
+    import torch
+
+    case = c5_case(n_inst=6)
+    want = oracle.score(case.bank, case.wrec, case.states, case.work)["psi"]
+    n = case.work.n_psi
+    dbank = runtime.DeviceBank(case.bank, case.weights)
+    ds, dw = dbank.upload_states(case.states), dbank.upload_work(case.work)
+    outs = [dbank.alloc_out(case.work, extras=False) for _ in range(6)]
+    streams = [torch.cuda.Stream() for _ in outs]
+    pipe = runtime.HostPipeline(dbank, case.states, case.work, n_chunks=3, graph=True)
+    torch.cuda.synchronize()
+    for _ in range(5):
+        for o, s in zip(outs, streams):
+            o.psi.fill_(0.0)
+        torch.cuda.synchronize()
+        for o, s in zip(outs, streams):
+            dbank.score_into(ds, dw, o, stream=s)
+        pipe.run()
+        torch.cuda.synchronize()
+        for o in outs:
+            assert np.array_equal(bits(o.psi.cpu().numpy()[:n]), bits(want))
+        assert np.array_equal(bits(pipe.host_psi.numpy()[:n]), bits(want))
+    pipe.close()
