@@ -247,6 +247,27 @@ def traffic_for(key: str):
         return None
 
 
+def issue_ceiling(key: str, ms: float, sm_mhz) -> dict | None:
+    """The binding ceiling of this gather/fp64 kernel: warp-instruction issue.
+    Instructions per launch come from the committed ncu capture
+    (profiles/ncu_instructions.json, smsp__inst_executed.sum); the peak is
+    148 SMs x 4 schedulers x 1 warp-instruction per cycle at the sampled SM
+    clock."""
+    path = os.path.join(ROOT, "profiles", "ncu_instructions.json")
+    try:
+        with open(path) as fh:
+            inst = json.load(fh).get(key)
+    except Exception:
+        inst = None
+    if not inst or not sm_mhz:
+        return None
+    peak = 148 * 4 * float(sm_mhz) * 1e6
+    achieved = inst / (ms / 1e3)
+    return {"bound": "issue", "warp_instructions_per_launch": inst,
+            "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "G warp-inst/s",
+            "frac": achieved / peak, "source": "profiles/ncu_instructions.json"}
+
+
 def time_device(torch, dbank, dstates, dwork, out, steps, warmup, flush, world, device,
                 gather=False, clocks=None):
     """Per-step kernel time (CUDA events on the launching stream), L2 flushed
@@ -508,6 +529,10 @@ def run_fate(args):
                 "traffic": traffic_for(key), "peak_source": peak_src,
                 "bytes_per_launch": nbytes, "bytes_per_candidate": nbytes / work.n_psi,
                 "kernel": "fate_score_kernel"}
+    csum = clocks.summary()
+    ceil = issue_ceiling(key, ms, csum.get("sm_mhz") or csum.get("sm_max_mhz"))
+    if ceil is not None:
+        roofline["issue_ceiling"] = ceil
 
     pipe = runtime.HostPipeline(dbank, states, work, extras=False, n_chunks=4, graph=True)
     e2e_ms, e2e_blocks = time_e2e(torch, pipe, max(10, args.steps), min(args.warmup, 3), world,
@@ -583,7 +608,10 @@ def measure_c4(torch, device, args) -> dict:
             "psi_per_step": work.n_psi,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": traffic_for("c4_sweep"),
-                         "bytes_per_launch": nbytes, "bytes_per_candidate": nbytes / work.n_psi},
+                         "bytes_per_launch": nbytes, "bytes_per_candidate": nbytes / work.n_psi,
+                         "issue_ceiling": issue_ceiling(
+                             "c4_sweep", ms, clocks.summary().get("sm_mhz")
+                             or clocks.summary().get("sm_max_mhz"))},
             "clocks": clocks.summary(), "gpu_launches": launches}
 
 

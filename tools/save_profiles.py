@@ -43,6 +43,16 @@ def main(src, tag):
     with open(os.path.join(prof, "ncu_traffic.json"), "w") as fh:
         json.dump(traffic, fh, indent=2)
     print(json.dumps(traffic))
+    # warp instructions per launch (issue-rate ceiling of the bench's roofline)
+    inst = {"_comment": f"smsp__inst_executed.sum (warp instructions) of one fate_score launch; "
+                        f"kernel {tag}"}
+    for k, key in (("c5", "c5_frontier"), ("c4", "c4_sweep")):
+        rep = os.path.join(src, f"{k}_full.ncu-rep")
+        if os.path.exists(rep):
+            inst[key] = int(float(ns.raw_metrics(rep)["smsp__inst_executed.sum"][0]))
+    with open(os.path.join(prof, "ncu_instructions.json"), "w") as fh:
+        json.dump(inst, fh, indent=2)
+    print(json.dumps(inst))
 
 
 if __name__ == "__main__":
