@@ -235,7 +235,7 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
                  const fate_out* out, cudaStream_t s) {
     if (!der->stage_rec || (win->levels > 0 && (!der->tmpl_ptr || !der->tmpl)))
         return fail(FATE_ENOTREADY, "v6 kernel needs stage records and op templates");
-    const V6Layout lay = SL ? v6_layout_static(win->max_level_ops)
+    const V6Layout lay = SL ? v6_layout_static<DPL>(win->max_level_ops)
                             : v6_layout(bank->n_devices, bank->max_queries, win->max_level_ops);
     const size_t smem = (size_t)lay.item_bytes * 4;
     if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v6 shared-memory footprint too large");
@@ -340,17 +340,14 @@ int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_window
     }
 }
 
-// Static shared-memory layout for D > 32 when the query batch fits V6S_B
-// (measured: C4 -4.5 %); for D <= 32 the larger static slice costs L1 capacity
-// the gathers need (C5 +4 %), so the runtime layout stays.  FATE_V6_DYNLAYOUT /
-// FATE_V6_STATICLAYOUT force one (A/B only).
+// Static shared-memory layout when the query batch fits it (V6Static<DPL>;
+// measured: C4 -4.5 %).  FATE_V6_DYNLAYOUT forces the runtime layout (A/B).
 template <int DPL>
 int launch_v6(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
               const fate_derived* der, const fate_state* st, const fate_work* work,
               const fate_out* out, cudaStream_t s) {
     static const bool dyn = getenv("FATE_V6_DYNLAYOUT") != nullptr;
-    static const bool stat = getenv("FATE_V6_STATICLAYOUT") != nullptr;
-    if (!dyn && (DPL == 2 || stat) && bank->max_queries <= V6S_B)
+    if (!dyn && bank->max_queries <= V6Static<DPL>::B)
         return launch_v6_sl<DPL, true>(bank, w, win, der, st, work, out, s);
     return launch_v6_sl<DPL, false>(bank, w, win, der, st, work, out, s);
 }

@@ -70,35 +70,44 @@ struct V6Layout {
     int rows, shard, aware, sw, tr, opval, opkey, key, cslot, rowdev;
 };
 
-// Static per-warp layout for the common shapes (query batch <= V6S_B, any
-// D <= 64): every field at a compile-time offset from the warp's slice base,
-// so the many shared-memory accesses use immediate offsets and the compiler's
-// rematerialisation under the register budget is a base re-derivation, not a
-// reload of runtime offsets.  The op buffers (size set by the windows) follow.
-constexpr int V6S_B = 32;
-struct __align__(16) V6SmemS {
-    double rows[V6_RCAP * V6S_B];
+// Static per-warp layouts for the common shapes: every field at a
+// compile-time offset from the warp's slice base, so the many shared-memory
+// accesses use immediate offsets and the compiler's rematerialisation under
+// the register budget is a base re-derivation, not a reload of runtime
+// offsets.  Sized per device-slot count: D <= 32 with query batches <= 16,
+// D <= 64 with batches <= 32.  The op buffers (size set by the windows)
+// follow the struct.
+template <int DMX, int BMX>
+struct __align__(16) V6SmemT {
+    double rows[V6_RCAP * BMX];
     double shard[V6_SLOTS * 2 * V6_KT];
     double aware[(V6_SLOTS + 1) & ~1];
-    double sw[FATE_MAX_DEVICES];
-    double tr[FATE_MAX_DEVICES];
-    int key[FATE_MAX_DEVICES];
-    int cslot[FATE_MAX_DEVICES];
+    double sw[DMX];
+    double tr[DMX];
+    int key[DMX];
+    int cslot[DMX];
     int rowdev[V6_RCAP];
 };
+template <int DPL>
+struct V6Static {
+    static constexpr int B = DPL == 1 ? 16 : 32;  // largest query batch
+    using T = V6SmemT<32 * DPL, B>;
+};
 
+template <int DPL>
 inline V6Layout v6_layout_static(int ops_cap) {
+    using S = typename V6Static<DPL>::T;
     V6Layout L{};
     const int ops4 = ((ops_cap > 0 ? ops_cap : 1) + 3) & ~3;
-    L.rows = (int)offsetof(V6SmemS, rows);
-    L.shard = (int)offsetof(V6SmemS, shard);
-    L.aware = (int)offsetof(V6SmemS, aware);
-    L.sw = (int)offsetof(V6SmemS, sw);
-    L.tr = (int)offsetof(V6SmemS, tr);
-    L.key = (int)offsetof(V6SmemS, key);
-    L.cslot = (int)offsetof(V6SmemS, cslot);
-    L.rowdev = (int)offsetof(V6SmemS, rowdev);
-    L.opval = (int)((sizeof(V6SmemS) + 15) & ~size_t(15));
+    L.rows = (int)offsetof(S, rows);
+    L.shard = (int)offsetof(S, shard);
+    L.aware = (int)offsetof(S, aware);
+    L.sw = (int)offsetof(S, sw);
+    L.tr = (int)offsetof(S, tr);
+    L.key = (int)offsetof(S, key);
+    L.cslot = (int)offsetof(S, cslot);
+    L.rowdev = (int)offsetof(S, rowdev);
+    L.opval = (int)((sizeof(S) + 15) & ~size_t(15));
     L.opkey = L.opval + 8 * ops4;
     L.item_bytes = (L.opkey + 4 * ops4 + 15) & ~15;
     return L;
@@ -350,7 +359,7 @@ __device__ __forceinline__ double v6_qc(const fate_bank& b, const fate_state& st
 // ---------------------------------------------------------------------------
 
 // One item (scenario, stage v) by one warp; sb = the warp's shared-memory slice
-// (static layout V6SmemS when SL, else the runtime layout `lay`).
+// (static layout V6Static<DPL>::T when SL, else the runtime layout `lay`).
 template <int DPL, bool OVR, bool SL>
 __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& w,
                                         const fate_windows& win, const fate_derived& der,
@@ -358,7 +367,8 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                                         const fate_out& out, const V6Layout& lay,
                                         const long long item, unsigned char* sb) {
     const int t = threadIdx.x & 31;
-    V6SmemS* const ss = reinterpret_cast<V6SmemS*>(sb);
+    using SMEM = typename V6Static<DPL>::T;
+    SMEM* const ss = reinterpret_cast<SMEM*>(sb);
     double* const s_rows = SL ? ss->rows : reinterpret_cast<double*>(sb + lay.rows);
     double* const s_shard = SL ? ss->shard : reinterpret_cast<double*>(sb + lay.shard);
     double* const s_aware = SL ? ss->aware : reinterpret_cast<double*>(sb + lay.aware);
@@ -372,7 +382,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 
     const unsigned FULL = 0xffffffffu;
     const int D = b.n_devices, LV = win.levels;
-    const int Bmax = SL ? V6S_B : b.max_queries;  // row stride of s_rows
+    const int Bmax = SL ? V6Static<DPL>::B : b.max_queries;  // row stride of s_rows
     const bool no_loc = w.ablation & FATE_NO_LOCALITY;
     const bool no_shard = w.ablation & FATE_NO_SHARD;
     const int H = w.eff_horizon;
