@@ -324,7 +324,10 @@ int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_window
                  const fate_out* out, cudaStream_t s) {
     const bool ovr = bank->has_overrides != 0;
     const char* e = getenv("FATE_MINB");
-    switch (e ? atoi(e) : (DPL == 1 ? 8 : 7)) {
+    // register budget (CTAs per SM), measured on B200: 10 for one device slot
+    // per lane (48 registers: the extra warps hide more latency than the
+    // spills cost; 8/9/12 were slower), 7 for two (72 registers, no spills)
+    switch (e ? atoi(e) : (DPL == 1 ? 10 : 7)) {
         case 1:
             return ovr ? launch_v6_mb<DPL, true, SL, 1>(bank, w, win, der, st, work, out, s)
                        : launch_v6_mb<DPL, false, SL, 1>(bank, w, win, der, st, work, out, s);
@@ -334,6 +337,9 @@ int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_window
         case 7:
             return ovr ? launch_v6_mb<DPL, true, SL, 7>(bank, w, win, der, st, work, out, s)
                        : launch_v6_mb<DPL, false, SL, 7>(bank, w, win, der, st, work, out, s);
+        case 10:
+            return ovr ? launch_v6_mb<DPL, true, SL, 10>(bank, w, win, der, st, work, out, s)
+                       : launch_v6_mb<DPL, false, SL, 10>(bank, w, win, der, st, work, out, s);
         default:
             return ovr ? launch_v6_mb<DPL, true, SL, 8>(bank, w, win, der, st, work, out, s)
                        : launch_v6_mb<DPL, false, SL, 8>(bank, w, win, der, st, work, out, s);
