@@ -534,196 +534,94 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 
     // ---- P1: row classes ------------------------------------------------------------------------
     // Devices with equal (sp, speed) share a bit-identical cache-aware row.
-    // Static classes (uniform speed, no query prefix groups): sp == P (A),
-    // sp == 0 < P (B), sp == P - t for a tabulated partial-hit count t
-    // (T0..T2).  Two formulations with the same result: for D > 32 each device
-    // finds its static class by value and only dynamic devices group by
-    // __match_any_sync (fewer ballots: C4 -4 %); for D <= 32 all devices group
-    // first and class representatives are tested (fewer live registers under
-    // the 64-register budget: C5 +3 % with the other form).
+    // Under uniform speed without query prefix groups a row depends on sp
+    // alone, so each device finds its *static* class by value -- sp == P (A),
+    // sp == 0 < P (B), sp == P - t for a tabulated partial-hit count t (T0..T2)
+    // -- and only the remaining (dynamic) devices group by __match_any_sync.
     int kb = 0, ki = 0, per = 0, n_rows = 0;
     bool kb_ok = false, ki_ok = false;
     unsigned long long dyn_m = 0ull;
     const bool uniform = b.flags & FATE_BANK_UNIFORM_SPEED;
     const int n_idle = __popcll(idle_m);
-    if (DPL == 2) {
-        if (R > 1 && !no_shard) {
-            kb = R < 1 + n_idle ? R : 1 + n_idle;
-            ki = R < n_idle ? R : n_idle;
+    if (R > 1 && !no_shard) {
+        kb = R < 1 + n_idle ? R : 1 + n_idle;
+        ki = R < n_idle ? R : n_idle;
+    }
+    kb_ok = kb >= 2 && kb <= V6_KT;
+    ki_ok = ki != kb && ki >= 2 && ki <= V6_KT;
+    per = 1 + (kb_ok ? kb : 0) + (ki_ok ? ki : 0);
+    const bool stat_ok = uniform && !per_device_rows && kb <= 2 && ki <= 2;
+    int rep[DPL];
+    bool dyn[DPL];
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+        int sl = -2;  // dynamic
+        if (stat_ok) {
+            const int c = cs[j], tt = it.Pv - c;
+            sl = c == it.Pv                                      ? 0
+                 : (c == 0 && it.Pv > 0)                         ? 1
+                 : (c > 0 && c < it.Pv && tokv.w > 0 && tt == tokv.x) ? 2
+                 : (c > 0 && c < it.Pv && tokv.w > 1 && tt == tokv.y) ? 3
+                 : (c > 0 && c < it.Pv && tokv.w > 2 && tt == tokv.z) ? 4
+                                                                 : -2;
         }
-        kb_ok = kb >= 2 && kb <= V6_KT;
-        ki_ok = ki != kb && ki >= 2 && ki <= V6_KT;
-        per = 1 + (kb_ok ? kb : 0) + (ki_ok ? ki : 0);
-        const bool stat_ok = uniform && !per_device_rows && kb <= 2 && ki <= 2;
-        int rep[DPL];
-        bool dyn[DPL];
-    #pragma unroll
-        for (int j = 0; j < DPL; ++j) {
-            int sl = -2;  // dynamic
-            if (stat_ok) {
-                const int c = cs[j], tt = it.Pv - c;
-                sl = c == it.Pv                                      ? 0
-                     : (c == 0 && it.Pv > 0)                         ? 1
-                     : (c > 0 && c < it.Pv && tokv.w > 0 && tt == tokv.x) ? 2
-                     : (c > 0 && c < it.Pv && tokv.w > 1 && tt == tokv.y) ? 3
-                     : (c > 0 && c < it.Pv && tokv.w > 2 && tt == tokv.z) ? 4
-                                                                     : -2;
+        if (ok[j] && sl >= 0) s_cslot[dv[j]] = sl;  // static class: slot known now
+        dyn[j] = ok[j] && sl == -2;
+        unsigned same = __ballot_sync(FULL, dyn[j]);
+        if (!per_device_rows) {
+            same &= __match_any_sync(FULL, cs[j]);
+            if (!uniform) {
+                const unsigned long long spd =
+                    __double_as_longlong(b.dev_speed[live[j] ? dv[j] : 0]);
+                same &= __match_any_sync(FULL, spd);
             }
-            if (ok[j] && sl >= 0) s_cslot[dv[j]] = sl;  // static class: slot known now
-            dyn[j] = ok[j] && sl == -2;
-            unsigned same = __ballot_sync(FULL, dyn[j]);
-            if (!per_device_rows) {
-                same &= __match_any_sync(FULL, cs[j]);
-                if (!uniform) {
-                    const unsigned long long spd =
-                        __double_as_longlong(b.dev_speed[live[j] ? dv[j] : 0]);
-                    same &= __match_any_sync(FULL, spd);
-                }
-            } else {
-                same &= 1u << t;
-            }
-            rep[j] = dyn[j] ? 32 * j + __ffs(same) - 1 : -1;
+        } else {
+            same &= 1u << t;
         }
-        if (DPL == 2 && !per_device_rows) {
-            // a slot-1 dynamic class may already exist among slot-0 devices
-            const unsigned reps0 = __ballot_sync(FULL, dyn[0] && rep[0] == dv[0]);
-            if (dyn[DPL - 1]) {
-                unsigned rr = reps0;
-                const double sp = b.dev_speed[dv[DPL - 1]];
-                #pragma unroll 1
-                while (rr) {
-                    const int e = __ffs(rr) - 1;
-                    rr &= rr - 1;
-                    if (s_key[e] == cs[DPL - 1] && (uniform || b.dev_speed[e] == sp)) {
-                        rep[DPL - 1] = e;
-                        break;
-                    }
+        rep[j] = dyn[j] ? 32 * j + __ffs(same) - 1 : -1;
+    }
+    if (DPL == 2 && !per_device_rows) {
+        // a slot-1 dynamic class may already exist among slot-0 devices
+        const unsigned reps0 = __ballot_sync(FULL, dyn[0] && rep[0] == dv[0]);
+        if (dyn[DPL - 1]) {
+            unsigned rr = reps0;
+            const double sp = b.dev_speed[dv[DPL - 1]];
+            #pragma unroll 1
+            while (rr) {
+                const int e = __ffs(rr) - 1;
+                rr &= rr - 1;
+                if (s_key[e] == cs[DPL - 1] && (uniform || b.dev_speed[e] == sp)) {
+                    rep[DPL - 1] = e;
+                    break;
                 }
             }
         }
-        // representatives of dynamic classes
-    #pragma unroll
-        for (int j = 0; j < DPL; ++j)
-            dyn_m |= (unsigned long long)__ballot_sync(FULL, dyn[j] && rep[j] == dv[j]) << (32 * j);
-        const int n_dyn = __popcll(dyn_m);
-        n_rows = n_dyn < V6_RCAP ? n_dyn : V6_RCAP;
-        // table slot of each device's class: 0 = A, 1 = B, 2..4 = T0..T2,
-        // V6_ROW0 + row slot, -1 = direct
-    #pragma unroll
-        for (int j = 0; j < DPL; ++j) {
-            if (!dyn[j]) continue;
-            const int r = __popcll(dyn_m & low_mask(rep[j]));
-            if (rep[j] == dv[j] && r < V6_RCAP) s_rowdev[r] = dv[j];
-            s_cslot[dv[j]] = r < V6_RCAP ? V6_ROW0 + r : -1;
-        }
-        if (stat_ok && t < 15) {
-            // lane t holds the sums of static class si = t / 3 (A, B, T0, T1, T2),
-            // entry e = t % 3 (full, k=2 shard 0, shard 1); written whether or not
-            // a device uses the class
-            const int si = t / 3, e = t - 3 * si;
-            if (e == 0) {
-                s_aware[si] = rsum;
-            } else {
-                if (kb == 2) s_shard[(si * 2 + 0) * V6_KT + (e - 1)] = rsum;
-                if (ki == 2 && ki != kb) s_shard[(si * 2 + 1) * V6_KT + (e - 1)] = rsum;
-            }
-        }
-    } else {
-        int rep[DPL];
-    #pragma unroll
-        for (int j = 0; j < DPL; ++j) {
-            unsigned same = (unsigned)(ok_m >> (32 * j));
-            if (!per_device_rows) {
-                same &= __match_any_sync(FULL, cs[j]);
-                if (!uniform) {
-                    const unsigned long long spd =
-                        __double_as_longlong(b.dev_speed[live[j] ? dv[j] : 0]);
-                    same &= __match_any_sync(FULL, spd);
-                }
-            } else {
-                same &= 1u << t;
-            }
-            rep[j] = ok[j] ? 32 * j + __ffs(same) - 1 : -1;
-        }
-        if (DPL == 2 && !per_device_rows) {
-            // a slot-1 class may already exist among slot-0 devices
-            const unsigned reps0 = __ballot_sync(FULL, ok[0] && rep[0] == dv[0]);
-            if (ok[DPL - 1]) {
-                unsigned rr = reps0;
-                const double sp = b.dev_speed[dv[DPL - 1]];
-                while (rr) {
-                    const int e = __ffs(rr) - 1;
-                    rr &= rr - 1;
-                    if (s_key[e] == cs[DPL - 1] && (uniform || b.dev_speed[e] == sp)) {
-                        rep[DPL - 1] = e;
-                        break;
-                    }
-                }
-            }
-        }
-        unsigned long long rep_m = 0ull;
-    #pragma unroll
-        for (int j = 0; j < DPL; ++j)
-            rep_m |= (unsigned long long)__ballot_sync(FULL, ok[j] && rep[j] == dv[j]) << (32 * j);
-        if (R > 1 && !no_shard) {
-            kb = R < 1 + n_idle ? R : 1 + n_idle;
-            ki = R < n_idle ? R : n_idle;
-        }
-        kb_ok = kb >= 2 && kb <= V6_KT;
-        ki_ok = ki != kb && ki >= 2 && ki <= V6_KT;
-        per = 1 + (kb_ok ? kb : 0) + (ki_ok ? ki : 0);
-        // static classes: representatives with sp == P (A), sp == 0 < P (B), and
-        // sp == P - t for a tabulated partial-hit token count t (T0..T2)
-        unsigned long long am = 0ull, bm = 0ull, tm[V6_NTOK] = {0ull, 0ull, 0ull};
-        if (uniform && !per_device_rows && kb <= 2 && ki <= 2) {
-    #pragma unroll
-            for (int j = 0; j < DPL; ++j) {
-                const bool r0 = ok[j] && rep[j] == dv[j];
-                am |= (unsigned long long)__ballot_sync(FULL, r0 && cs[j] == it.Pv) << (32 * j);
-                bm |= (unsigned long long)__ballot_sync(FULL, r0 && cs[j] == 0 && it.Pv > 0) << (32 * j);
-                const int tt = it.Pv - cs[j];  // cached tokens behind this class
-                const bool part = r0 && cs[j] > 0 && cs[j] < it.Pv;
-                tm[0] |= (unsigned long long)__ballot_sync(FULL, part && tokv.w > 0 && tt == tokv.x) << (32 * j);
-                tm[1] |= (unsigned long long)__ballot_sync(FULL, part && tokv.w > 1 && tt == tokv.y) << (32 * j);
-                tm[2] |= (unsigned long long)__ballot_sync(FULL, part && tokv.w > 2 && tt == tokv.z) << (32 * j);
-            }
-        }
-        // representatives of dynamic classes
-        dyn_m = rep_m & ~am & ~bm & ~tm[0] & ~tm[1] & ~tm[2];
-        const int n_dyn = __popcll(dyn_m);
-        n_rows = n_dyn < V6_RCAP ? n_dyn : V6_RCAP;
-        // table slot of each device's class: 0 = A, 1 = B, 2..4 = T0..T2,
-        // V6_ROW0 + row slot, -1 = direct
-    #pragma unroll
-        for (int j = 0; j < DPL; ++j) {
-            if (!ok[j]) continue;
-            const unsigned long long rb = 1ull << rep[j];
-            int slot;
-            if (am & rb) slot = 0;
-            else if (bm & rb) slot = 1;
-            else if (tm[0] & rb) slot = 2;
-            else if (tm[1] & rb) slot = 3;
-            else if (tm[2] & rb) slot = 4;
-            else {
-                const int r = __popcll(dyn_m & low_mask(rep[j]));
-                slot = r < V6_RCAP ? V6_ROW0 + r : -1;
-                if (rep[j] == dv[j] && r < V6_RCAP) s_rowdev[r] = dv[j];
-            }
-            s_cslot[dv[j]] = slot;
-        }
-        if (t < 15) {
-            // lane t holds the sums of static class si = t / 3 (A, B, T0, T1, T2),
-            // entry e = t % 3 (full, k=2 shard 0, shard 1)
-            const int si = t / 3, e = t - 3 * si;
-            const unsigned long long cm = si == 0 ? am : si == 1 ? bm : tm[si - 2];
-            if (cm != 0ull) {
-                if (e == 0) {
-                    s_aware[si] = rsum;
-                } else {
-                    if (kb == 2) s_shard[(si * 2 + 0) * V6_KT + (e - 1)] = rsum;
-                    if (ki == 2 && ki != kb) s_shard[(si * 2 + 1) * V6_KT + (e - 1)] = rsum;
-                }
-            }
+    }
+    // representatives of dynamic classes
+#pragma unroll
+    for (int j = 0; j < DPL; ++j)
+        dyn_m |= (unsigned long long)__ballot_sync(FULL, dyn[j] && rep[j] == dv[j]) << (32 * j);
+    const int n_dyn = __popcll(dyn_m);
+    n_rows = n_dyn < V6_RCAP ? n_dyn : V6_RCAP;
+    // table slot of each device's class: 0 = A, 1 = B, 2..4 = T0..T2,
+    // V6_ROW0 + row slot, -1 = direct
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+        if (!dyn[j]) continue;
+        const int r = __popcll(dyn_m & low_mask(rep[j]));
+        if (rep[j] == dv[j] && r < V6_RCAP) s_rowdev[r] = dv[j];
+        s_cslot[dv[j]] = r < V6_RCAP ? V6_ROW0 + r : -1;
+    }
+    if (stat_ok && t < 15) {
+        // lane t holds the sums of static class si = t / 3 (A, B, T0, T1, T2),
+        // entry e = t % 3 (full, k=2 shard 0, shard 1); written whether or not
+        // a device uses the class
+        const int si = t / 3, e = t - 3 * si;
+        if (e == 0) {
+            s_aware[si] = rsum;
+        } else {
+            if (kb == 2) s_shard[(si * 2 + 0) * V6_KT + (e - 1)] = rsum;
+            if (ki == 2 && ki != kb) s_shard[(si * 2 + 1) * V6_KT + (e - 1)] = rsum;
         }
     }
     __syncwarp();
