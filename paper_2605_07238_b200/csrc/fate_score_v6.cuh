@@ -74,9 +74,9 @@ struct V6Layout {
 // compile-time offset from the warp's slice base, so the many shared-memory
 // accesses use immediate offsets and the compiler's rematerialisation under
 // the register budget is a base re-derivation, not a reload of runtime
-// offsets.  Sized per device-slot count: D <= 32 with query batches <= 16,
-// D <= 64 with batches <= 32.  The op buffers (size set by the windows)
-// follow the struct.
+// offsets.  Sized per device-slot count for query batches <= 16 (larger
+// batches use the runtime layout).  The op buffers (size set by the longest
+// op template) follow the struct.
 template <int DMX, int BMX>
 struct __align__(16) V6SmemT {
     double rows[V6_RCAP * BMX];
@@ -90,7 +90,7 @@ struct __align__(16) V6SmemT {
 };
 template <int DPL>
 struct V6Static {
-    static constexpr int B = DPL == 1 ? 16 : 32;  // largest query batch
+    static constexpr int B = 16;  // largest query batch (configs 1-5 use 16 / 32)
     using T = V6SmemT<32 * DPL, B>;
 };
 
