@@ -505,7 +505,10 @@ def run_fate(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample_rate(bank, cfg.weights, states, work, target_s=args.cpu_seconds)
 
+    t_bank = time.perf_counter()
     dbank = runtime.DeviceBank(bank, cfg.weights, device=device)
+    torch.cuda.synchronize(device)
+    bank_setup_s = time.perf_counter() - t_bank  # once per (bank, weights), not per step
     dstates = dbank.upload_states(states)
     dwork = dbank.upload_work(work)
     out = dbank.alloc_out(work, extras=True)
@@ -566,6 +569,7 @@ def run_fate(args):
                 "horizon": cfg.weights.horizon, "psi_per_gpu_step": work.n_psi,
                 "work_items_per_gpu_step": work.n_items,
                 "l2": "flushed between steps (256 MiB write, outside the events)",
+                "bank_setup_s": round(bank_setup_s, 3),
                 "parallelism": f"dp{world}: instances sharded by rank, no data-path collective"
                                + (" + NCCL all-gather of Psi" if args.gather else ""),
             },
