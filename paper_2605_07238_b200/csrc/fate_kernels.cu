@@ -259,14 +259,15 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
         occ_dev = dev;
         occ_fn = fn;
     }
-    // items per ticket: guided (0) for one device slot per lane, 1 for two
-    // (heavier items: finer tail balance beats fewer atomics; measured on B200)
+    // items per ticket: 2 for one device slot per lane, 1 for two (heavier
+    // items: finer tail balance beats fewer atomics); 0 = guided sizes.
+    // Measured on B200 at the current register budgets.
     static int fetch_env = -2;
     if (fetch_env == -2) {
         const char* e = getenv("FATE_V6_FETCH");
         fetch_env = e ? std::max(0, std::min(64, atoi(e))) : -1;
     }
-    const int fetch = fetch_env >= 0 ? fetch_env : (DPL == 1 ? 0 : 1);
+    const int fetch = fetch_env >= 0 ? fetch_env : (DPL == 1 ? 2 : 1);
     if (work->n_items > 0x7fffffffLL - 4 * 128 * 64)
         return fail(FATE_ETOOBIG, "v6: too many items for the 32-bit ticket counter");
     const long long want = (work->n_items + 3) / 4;
