@@ -530,7 +530,7 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
         if (out->stage_rec) {
             if (!out->split_penalty || !out->inst_qgroups)
                 return fail(FATE_EINVAL, "stage records need split_penalty and inst_qgroups");
-            fate_prepare_stagerec_kernel<<<blocks, threads, 0, s>>>(*bank, *w, *out);
+            fate_prepare_stagerec_kernel<<<blocks, threads, 0, s>>>(*bank, *w, *win, *out);
             g_launches++;
             if ((rc = cuda_status("fate_prepare_stagerec_kernel"))) return rc;
         }

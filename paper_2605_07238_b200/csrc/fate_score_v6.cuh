@@ -50,7 +50,8 @@ struct __align__(16) V6Stage {
     int pa0, pa1, q0, nq;          // parent CSR range, query range
     int stage_off, flags, bound, n_elig;  // instance's first stage, V6_*, slots, |A(v)|
     unsigned long long elig;       // eligible-device mask
-    int role, pad;
+    int role, minlvl;              // role row; lowest window-parent level of any horizon
+                                   // level (INT_MAX: no window parent)
     double pcoef, pscale;          // prefill coeff (1.0 without model), role prefill scale
     double decode, cplx;           // out * decode coeff * decode scale, role complexity
     double swv, split;             // switch cost if switching, slot>=1 split penalty
@@ -143,7 +144,8 @@ inline V6Layout v6_layout(int D, int Bmax, int ops_cap) {
 
 // One thread per stage: the stage record (after fate_prepare_stage_kernel,
 // which produced split_penalty and inst_qgroups).
-__global__ void fate_prepare_stagerec_kernel(fate_bank b, fate_weights w, fate_derived der) {
+__global__ void fate_prepare_stagerec_kernel(fate_bank b, fate_weights w, fate_windows win,
+                                             fate_derived der) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= b.n_stages) return;
     V6Stage r;
@@ -163,7 +165,11 @@ __global__ void fate_prepare_stagerec_kernel(fate_bank b, fate_weights w, fate_d
     r.n_elig = __popcll(r.elig);
     r.bound = (w.ablation & FATE_NO_SHARD) ? 1 : (r.R < r.n_elig ? r.R : r.n_elig);
     r.role = b.st_role[g];
-    r.pad = 0;
+    r.minlvl = 0x7fffffff;
+    for (int l = 0; l < win.levels; ++l) {
+        const int x = win.wpar_minlvl[(long long)g * win.levels + l];
+        r.minlvl = x < r.minlvl ? x : r.minlvl;
+    }
     const int ri = r.role;
     r.pcoef = r.m >= 0 ? b.model_prefill[r.m] : 1.0;
     const double dcoef = r.m >= 0 ? b.model_decode[r.m] : 0.0;
@@ -450,9 +456,10 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             const int r = res0[j];
             tail_full[j] = row[(r != -1 && r != m && r < b.n_models) ? 1 + r : 0];
         }
-        if (!no_loc) {
+        if (!no_loc && (int)(h3.y >> 32) <= done_lvl) {
             // a window parent above the scenario's highest located stage cannot be
-            // located: levels whose parents all lie above it need no gather
+            // located: levels whose parents all lie above it need no gather (the
+            // stage record's minimum over the levels skips the whole loop)
             #pragma unroll 1
             for (int l = 0; l < LV; ++l) {
                 const long long vl = (long long)v * LV + l;
