@@ -188,15 +188,17 @@ def build_c5(rank: int, world: int, mode: str):
     return cfg, fb.bank, fb.states, work, plan
 
 
-def build_c4(mode: str = "sweep", n_scen: int = C4_SCENARIOS):
+def build_c4(mode: str = "sweep", n_scen: int = C4_SCENARIOS, first_scen: int = 0):
     """Config 4 from the native generator: one 10k-stage instance (seed 1),
-    scenario states s = 0..n_scen-1."""
+    scenario states s = first_scen .. first_scen+n_scen-1 (ranks shard the
+    scenario seeds)."""
     import numpy as np
 
     from paper_2605_07238_b200 import fastgen, pack, scenarios
 
     cfg = scenarios.config_c4_catalog()
-    parts = [fastgen.synth_batch(cfg, 1, 1, s, 100, 100, 0.03, 16) for s in range(n_scen)]
+    parts = [fastgen.synth_batch(cfg, 1, 1, s, 100, 100, 0.03, 16)
+             for s in range(first_scen, first_scen + n_scen)]
     bank = parts[0].bank
     cap = max(p.states.kappa_cap for p in parts)
     arrays = {}
@@ -498,7 +500,7 @@ def run_fate(args):
     if args.workload == "c5":
         cfg, bank, states, work, plan = build_c5(rank, world, args.mode)
     else:
-        cfg, bank, states, work = build_c4(args.mode)
+        cfg, bank, states, work = build_c4(args.mode, first_scen=rank * C4_SCENARIOS)
         plan = None
 
     cpu = None
@@ -570,7 +572,9 @@ def run_fate(args):
                 "work_items_per_gpu_step": work.n_items,
                 "l2": "flushed between steps (256 MiB write, outside the events)",
                 "bank_setup_s": round(bank_setup_s, 3),
-                "parallelism": f"dp{world}: instances sharded by rank, no data-path collective"
+                "parallelism": f"dp{world}: "
+                               + ("instances" if args.workload == "c5" else "scenario seeds")
+                               + " sharded by rank, no data-path collective"
                                + (" + NCCL all-gather of Psi" if args.gather else ""),
             },
             "roofline": roofline,
