@@ -46,6 +46,7 @@ struct fate_pipeline {
     cudaStream_t cap = nullptr;
     cudaGraphExec_t exec = nullptr;
     long long launches_per_replay = 0;
+    bool invalidated = false;  // a later call outgrew the captured workspaces
     // device workspaces (grown on demand): wire-format staging + the SoA the
     // kernels read
     struct Buf {
@@ -67,8 +68,14 @@ int cuda_fail(cudaError_t e, const char* what) {
     return fate_internal_fail((int)e, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-int grow(fate_pipeline::Buf& b, size_t bytes) {
+int grow(fate_pipeline* p, fate_pipeline::Buf& b, size_t bytes) {
     if (bytes <= b.cap) return 0;
+    if (p->exec) {
+        // a captured graph addresses the old workspaces: it must be recaptured
+        cudaGraphExecDestroy(p->exec);
+        p->exec = nullptr;
+        p->invalidated = true;
+    }
     if (b.p) cudaFree(b.p);
     b.p = nullptr;
     b.cap = 0;
@@ -205,19 +212,19 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
     p->d2h_bytes = 0;
 
     int rc;
-    if ((rc = grow(p->rec, RB * (size_t)S)) || (rc = grow(p->items, 16 * (size_t)W)) ||
-        (rc = grow(p->scen_inst, 4 * (size_t)S)) || (rc = grow(p->scen_clock, 8 * (size_t)S)) ||
-        (rc = grow(p->scen_loc_off, 8 * (size_t)S)) ||
-        (rc = grow(p->scen_done_level, 4 * (size_t)S)) ||
-        (rc = grow(p->loc, 4 * (size_t)hb->n_loc)) || (rc = grow(p->loc8, (size_t)hb->n_loc)) ||
-        (rc = grow(p->residency, 4 * (size_t)S * D)) ||
-        (rc = grow(p->dev_free, 8 * (size_t)S * D)) || (rc = grow(p->kappa_n, 4 * (size_t)S * D)) ||
-        (rc = grow(p->kappa, 16 * (size_t)S * D * cap)) || (rc = grow(p->w_scen, 4 * (size_t)W)) ||
-        (rc = grow(p->w_stage, 4 * (size_t)W)) || (rc = grow(p->w_psi_off, 8 * (size_t)W)) ||
-        (rc = grow(p->psi, 8 * (size_t)hb->n_psi)))
+    if ((rc = grow(p, p->rec, RB * (size_t)S)) || (rc = grow(p, p->items, 16 * (size_t)W)) ||
+        (rc = grow(p, p->scen_inst, 4 * (size_t)S)) || (rc = grow(p, p->scen_clock, 8 * (size_t)S)) ||
+        (rc = grow(p, p->scen_loc_off, 8 * (size_t)S)) ||
+        (rc = grow(p, p->scen_done_level, 4 * (size_t)S)) ||
+        (rc = grow(p, p->loc, 4 * (size_t)hb->n_loc)) || (rc = grow(p, p->loc8, (size_t)hb->n_loc)) ||
+        (rc = grow(p, p->residency, 4 * (size_t)S * D)) ||
+        (rc = grow(p, p->dev_free, 8 * (size_t)S * D)) || (rc = grow(p, p->kappa_n, 4 * (size_t)S * D)) ||
+        (rc = grow(p, p->kappa, 16 * (size_t)S * D * cap)) || (rc = grow(p, p->w_scen, 4 * (size_t)W)) ||
+        (rc = grow(p, p->w_stage, 4 * (size_t)W)) || (rc = grow(p, p->w_psi_off, 8 * (size_t)W)) ||
+        (rc = grow(p, p->psi, 8 * (size_t)hb->n_psi)))
         return rc;
-    if (sched_host && (rc = grow(p->sched, 8 * (size_t)W * D))) return rc;
-    if (completion_host && (rc = grow(p->completion, 8 * (size_t)W * D))) return rc;
+    if (sched_host && (rc = grow(p, p->sched, 8 * (size_t)W * D))) return rc;
+    if (completion_host && (rc = grow(p, p->completion, 8 * (size_t)W * D))) return rc;
     if (mode == Mode::size_only) return 0;
 
     fate_state dst{};
@@ -416,6 +423,7 @@ int fate_pipeline_capture(fate_pipeline* p, const fate_bank* bank, const fate_we
         cudaGraphExecDestroy(p->exec);
         p->exec = nullptr;
     }
+    p->invalidated = false;
     cudaError_t e;
     if (!p->cap && (e = cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking)) != cudaSuccess)
         return cuda_fail(e, "fate_pipeline_capture: stream");
@@ -446,7 +454,12 @@ int fate_pipeline_capture(fate_pipeline* p, const fate_bank* bank, const fate_we
 }
 
 int fate_pipeline_replay(fate_pipeline* p, void* stream) {
-    if (!p || !p->exec) return fate_internal_fail(FATE_ENOTREADY, "fate_pipeline_replay: nothing captured");
+    if (!p || !p->exec)
+        return fate_internal_fail(FATE_ENOTREADY,
+                                  p && p->invalidated
+                                      ? "fate_pipeline_replay: workspaces reallocated by a larger "
+                                        "batch since the capture; capture again"
+                                      : "fate_pipeline_replay: nothing captured");
     cudaError_t e = cudaGraphLaunch(p->exec, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "fate_pipeline_replay");
     fate_internal_count_launches(p->launches_per_replay);

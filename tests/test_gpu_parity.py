@@ -216,3 +216,31 @@ def test_concurrent_launches_on_streams_and_graph_replay():
             assert np.array_equal(bits(o.psi.cpu().numpy()[:n]), bits(want))
         assert np.array_equal(bits(pipe.host_psi.numpy()[:n]), bits(want))
     pipe.close()
+
+
+def test_captured_pipeline_invalidated_by_larger_batch():
+    """A direct call that outgrows the captured workspaces invalidates the
+    graph: replay then refuses (status < 0) instead of using freed memory;
+    a new capture works."""
+    import ctypes as C
+
+    import torch
+
+    small, big = c5_case(n_inst=2), c5_case(n_inst=6)
+    dbank = runtime.DeviceBank(big.bank, big.weights)
+    sub = pack.make_work(big.bank, [(s, g) for s, g in zip(big.work.scen, big.work.stage)
+                                    if s < 2], False)
+    pipe = runtime.HostPipeline(dbank, big.states, sub, n_chunks=2, graph=True)
+    other = runtime.HostPipeline(dbank, big.states, big.work, n_chunks=2)
+    L = runtime.load_library()
+    s = torch.cuda.current_stream()
+    rc = L.fate_pipeline_score(pipe.handle, C.byref(dbank.cbank), C.byref(dbank.cweights),
+                               C.byref(dbank.cwin), C.byref(dbank.cder), C.byref(other.batch),
+                               C.c_void_p(other.host_psi.data_ptr()), None, None,
+                               C.c_void_p(s.cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError, match="capture again"):
+        pipe.run()
+    other.close()
+    pipe.close()
