@@ -810,7 +810,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     }
 
     // ---- P4: per-device assembly ----------------------------------------------------------------
-    // Shard bound R = 2 with every class tabulated (one device slot per lane):
+    // Shard bound R = 2 with every class tabulated:
     // a device's second shard always goes to the first idle device other than
     // itself, so each device's shard-1 total sw + tr + shard sum is computed
     // once and the two candidates (first / second idle device) are shuffled --
@@ -819,17 +819,28 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     bool fast2 = false;
     double t1_e1 = 0.0, t1_e2 = 0.0;
     int e1 = -1, e2 = -1;
-    if (DPL == 1 && R == 2 && !no_shard && kb == 2) {
-        const int sl = ok[0] ? s_cslot[dv[0]] : 0;
-        fast2 = __all_sync(FULL, sl >= 0);
+    if (R == 2 && !no_shard && kb == 2) {
+        int sl[DPL];
+        bool all_tab = true;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) {
+            sl[j] = ok[j] ? s_cslot[dv[j]] : 0;
+            all_tab = all_tab && sl[j] >= 0;
+        }
+        fast2 = __all_sync(FULL, all_tab);
         if (fast2) {
-            const double t1self =
-                ok[0] ? s_sw[dv[0]] + s_tr[dv[0]] + s_shard[(sl * 2 + 0) * V6_KT + 1] : 0.0;
+            double t1self[DPL];
+#pragma unroll
+            for (int j = 0; j < DPL; ++j)
+                t1self[j] = ok[j] ? s_sw[dv[j]] + s_tr[dv[j]] +
+                                        s_shard[(sl[j] * 2 + 0) * V6_KT + 1]
+                                  : 0.0;
             e1 = idle_m ? __ffsll((long long)idle_m) - 1 : 0;
             const unsigned long long r2 = idle_m & (idle_m - 1ull);
             e2 = r2 ? __ffsll((long long)r2) - 1 : 0;
-            t1_e1 = __shfl_sync(FULL, t1self, e1 & 31);
-            t1_e2 = __shfl_sync(FULL, t1self, e2 & 31);
+            // device e lives in lane e % 32, slot e / 32 (warp-uniform choice)
+            t1_e1 = __shfl_sync(FULL, (DPL > 1 && e1 >= 32) ? t1self[DPL - 1] : t1self[0], e1 & 31);
+            t1_e2 = __shfl_sync(FULL, (DPL > 1 && e2 >= 32) ? t1self[DPL - 1] : t1self[0], e2 & 31);
         }
     }
     double* psi = out.psi + work.psi_off[item];
