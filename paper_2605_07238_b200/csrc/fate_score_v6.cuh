@@ -460,16 +460,15 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             // a window parent above the scenario's highest located stage cannot be
             // located: levels whose parents all lie above it need no gather (the
             // stage record's minimum over the levels skips the whole loop)
+            // A level whose lowest window parent is at or below that level is
+            // walked without first checking that a parent is actually located:
+            // with no located parent the walk over its op template is the
+            // static chain itself (same ops, same order), so the outcome is
+            // identical either way and the extra gather pass is saved.
             #pragma unroll 1
             for (int l = 0; l < LV; ++l) {
                 const long long vl = (long long)v * LV + l;
-                if (win.wpar_minlvl[vl] > done_lvl) continue;
-                const long long w1 = win.wpar_ptr[vl + 1];
-                bool located = false;
-                #pragma unroll 1
-                for (long long i = win.wpar_ptr[vl] + t; i < w1; i += 32)
-                    located |= loc_row[win.wpar_idx[i]] >= 0;
-                if (__any_sync(FULL, located)) walk_m |= 1u << (l < 31 ? l : 31);
+                if (win.wpar_minlvl[vl] <= done_lvl) walk_m |= 1u << (l < 31 ? l : 31);
             }
         }
     }
