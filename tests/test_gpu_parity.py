@@ -244,3 +244,29 @@ def test_captured_pipeline_invalidated_by_larger_batch():
         pipe.run()
     other.close()
     pipe.close()
+
+
+def test_c4_full_sweep_scenario_and_c5_full_frontier():
+    """Full-size parity: every stage of a config-4 scenario (10 000 stages x
+    64 devices x <= 2 slots, ~1.1 M Psi) and the full config-5 frontier of
+    512 instances (~0.7 M Psi), each bit-identical to the oracle."""
+    import bench
+    from paper_2605_07238_b200 import fastgen, scenarios
+
+    cfg, bank, states, work = bench.build_c4("sweep", n_scen=1, first_scen=2)
+    want = oracle.score(bank, pack.weights_record(cfg.weights), states, work,
+                        with_extras=False)["psi"]
+    dbank = runtime.DeviceBank(bank, cfg.weights)
+    got = dbank.score(states, work, extras=False).psi.cpu().numpy()[: work.n_psi]
+    assert work.n_psi > 1_000_000
+    assert np.array_equal(bits(got), bits(want))
+
+    cfg5 = scenarios.config_c5()
+    fb = fastgen.synth_batch(cfg5, 512, 1000, 0, 20, 25, 0.12, 16)
+    sc, g = fb.frontier_items()
+    work5 = pack.make_work(fb.bank, zip(sc.tolist(), g.tolist()), False)
+    want5 = oracle.score(fb.bank, pack.weights_record(cfg5.weights), fb.states, work5,
+                         with_extras=False)["psi"]
+    d5 = runtime.DeviceBank(fb.bank, cfg5.weights)
+    got5 = d5.score(fb.states, work5, extras=False).psi.cpu().numpy()[: work5.n_psi]
+    assert np.array_equal(bits(got5), bits(want5))
