@@ -284,6 +284,71 @@ def bound_of(bank: PackedBank, g: int, no_shard: bool) -> int:
 # ---------------------------------------------------------------------------
 
 
+# ---------------------------------------------------------------------------
+# binary bank format: pack once, score many
+# ---------------------------------------------------------------------------
+
+BANK_FORMAT = "fate.bank@1"
+
+
+def _json_default(x):
+    if isinstance(x, np.integer):
+        return int(x)
+    if isinstance(x, np.floating):
+        return float(x)
+    raise TypeError(f"{type(x).__name__} is not serialisable")
+
+
+def save_bank(bank: PackedBank, path) -> None:
+    """Write the packed static side as one ``.npz``: every ``fate_bank``
+    array verbatim plus the index dictionaries, so a batch packed once (from
+    instance JSON or the generators) is reloaded without touching the
+    instance objects.  Horizon windows are not stored; the native builder
+    derives them from the CSR on first use."""
+    import json
+
+    ids = [sid for per_inst in bank.stage_ids for sid in per_inst]
+    if any("\n" in sid for sid in ids):
+        raise ValueError("stage ids containing a newline cannot be stored")
+    meta = dict(format=BANK_FORMAT, device_ids=list(bank.device_ids),
+                model_index=bank.model_index, n_models=bank.n_models,
+                group_index=bank.group_index, scalars=bank.scalars,
+                n_stage_ids=[len(s) for s in bank.stage_ids])
+    blobs = {f"a.{k}": np.ascontiguousarray(v) for k, v in bank.arrays.items()}
+    blobs["meta"] = np.frombuffer(json.dumps(meta, default=_json_default).encode(), np.uint8)
+    blobs["ids"] = np.frombuffer("\n".join(ids).encode(), np.uint8)
+    with open(path, "wb") as fh:
+        np.savez(fh, **blobs)
+
+
+def load_bank(path) -> PackedBank:
+    """Inverse of :func:`save_bank`; ``instances`` is empty on the result."""
+    import json
+
+    with np.load(path, allow_pickle=False) as z:
+        meta = json.loads(bytes(z["meta"]).decode())
+        if meta.get("format") != BANK_FORMAT:
+            raise ValueError(f"unsupported bank format {meta.get('format')!r}")
+        arrays = {k[2:]: z[k] for k in z.files if k.startswith("a.")}
+        flat = bytes(z["ids"]).decode().split("\n") if z["ids"].size else []
+    stage_ids = []
+    pos = 0
+    for n in meta["n_stage_ids"]:
+        stage_ids.append(flat[pos: pos + n])
+        pos += n
+    if pos != len(flat):
+        raise ValueError("bank file: stage id table does not match the instance sizes")
+    device_ids = list(meta["device_ids"])
+    return PackedBank(
+        device_ids=device_ids, dev_index={d: i for i, d in enumerate(device_ids)},
+        model_index=dict(meta["model_index"]), n_models=int(meta["n_models"]),
+        group_index=dict(meta["group_index"]), arrays=arrays, scalars=dict(meta["scalars"]),
+        instances=[], stage_ids=stage_ids,
+        stage_index=[{sid: i for i, sid in enumerate(ids)} for ids in stage_ids],
+        inst_stage_off=arrays["inst_stage_off"],
+    )
+
+
 @dataclass
 class PackedStates:
     arrays: dict

@@ -77,6 +77,28 @@ def test_generators_match_reference(reference):
     assert MB.stable_hash64_many(keys) == [MB.stable_hash64(k) for k in keys]
 
 
+def test_instance_json_matches_reference_serialiser(reference):
+    """Mirror writer == reference writer, text for text; each reader accepts
+    the other's output (model.py:322-422)."""
+    import wfsched.benchgen as RB
+    import wfsched.model as RM
+
+    from paper_2605_07238_b200.wf import instance_io as IO
+
+    cfg5 = scenarios.config_c5()
+    pairs = [(RB.make_instance(RB.synth_generate(RB.SuiteSpec(
+        kind="synthetic", depth=20, width=25, density=0.12, seed=1000 + i), cfg5), 16, 1000 + i),
+        scenarios.c5_instance(i, cfg5)) for i in (0, 7)]
+    rc, mc = __import__("wfsched.config").config.default_config(4), MC.default_config(4)
+    pairs += list(zip(RB.build_prefix_suite(RB.SuiteSpec(kind="prefix_reuse", repeat_ratio=0.25), rc),
+                      MB.build_prefix_suite(MB.SuiteSpec(kind="prefix_reuse", repeat_ratio=0.25), mc)))
+    for ref_inst, mir_inst in pairs:
+        text = RM.instance_to_json(ref_inst)
+        assert IO.instance_to_json(mir_inst) == text
+        assert IO.instance_to_json(IO.instance_from_json(text)) == text
+        assert RM.instance_to_json(RM.instance_from_json(IO.instance_to_json(mir_inst))) == text
+
+
 def test_solver_matches_reference_verification_problems(reference):
     from wfsched import planner as RP
     from wfsched.verification import random_problem
