@@ -73,3 +73,22 @@ def test_c45_sampled(scorer):
 
 def test_c5_assignments_budget0(scorer):
     assert GC.check_c5_assign(gpu=True) == 16
+
+
+def test_c1_from_reference_instance_json(scorer):
+    """The config-1 instance as the reference CLI writes it to disk
+    (tests/golden/instances/c1.json) replays the golden default run."""
+    import os
+
+    from paper_2605_07238_b200.wf import instance_io as IO
+
+    runs, arrs = G.load("c1")
+    r = next(x for x in runs if x["variant"]["tag"] == "default")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "instances",
+                        "c1.json")
+    with open(path) as fh:
+        inst = IO.instance_from_json(fh.read())
+    _, cfg = G.c1_setup(r["variant"])
+    _, problems, n_psi = G.replay(r, arrs, inst, cfg, scorer)
+    assert not problems, problems[:3]
+    assert n_psi > 0

@@ -78,6 +78,16 @@ def test_c5_sweep():
     assert_parity(c5_case(n_inst=2, first=10, sweep=True))
 
 
+def test_bank_file_scores_like_the_packed_bank(tmp_path):
+    """A bank reloaded from its ``fate.bank@1`` file (no instance objects)
+    scores bit-identically to the oracle."""
+    case = edge_case(horizon=3)
+    pack.save_bank(case.bank, tmp_path / "bank.npz")
+    case.bank = pack.load_bank(tmp_path / "bank.npz")
+    assert case.bank.instances == []
+    assert_parity(case)
+
+
 def test_c4_frontier_and_sweep_sample():
     assert_parity(c4_case(scen=(0, 3), sweep_stride=97))
 
