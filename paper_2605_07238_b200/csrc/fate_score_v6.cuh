@@ -372,7 +372,8 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                                         const fate_state& st, const fate_work& work,
                                         const fate_out& out, const V6Layout& lay,
                                         const long long item, unsigned char* sb) {
-    const int t = threadIdx.x & 31;
+    int t;
+    asm("mov.u32 %0, %%laneid;" : "=r"(t));
     using SMEM = typename V6Static<DPL>::T;
     SMEM* const ss = reinterpret_cast<SMEM*>(sb);
     double* const s_rows = SL ? ss->rows : reinterpret_cast<double*>(sb + lay.rows);
@@ -1003,7 +1004,8 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
                                                                   V6Layout lay, int qslot,
                                                                   int fetch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int wi = threadIdx.x >> 5, t = threadIdx.x & 31;
+    const int t = threadIdx.x & 31;
+    const int wi = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     unsigned int* q = g_v6_queue + 2 * qslot;
     const long long n = work.n_items;
     unsigned char* sb = smem_raw + lay.item_bytes * wi;
