@@ -235,8 +235,17 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
                  const fate_out* out, cudaStream_t s) {
     if (!der->stage_rec || (win->levels > 0 && (!der->tmpl_ptr || !der->tmpl)))
         return fail(FATE_ENOTREADY, "v6 kernel needs stage records and op templates");
-    const V6Layout lay = SL ? v6_layout_static<DPL>(win->max_level_ops)
-                            : v6_layout(bank->n_devices, bank->max_queries, win->max_level_ops);
+    static int opcap_env = -1;
+    if (opcap_env < 0) {
+        const char* e = getenv("FATE_V6_OPCAP");
+        opcap_env = e ? std::max(32, std::min(4096, atoi(e))) & ~3 : 0;
+    }
+    const int opcap = opcap_env > 0 ? opcap_env : v6_opcap_default<DPL>();
+    constexpr bool maskw = !OVR && DPL == 2;
+    const V6Layout lay =
+        SL ? v6_layout_static<DPL>(win->max_level_ops, bank->n_models, maskw, opcap)
+           : v6_layout(bank->n_devices, bank->max_queries, win->max_level_ops, bank->n_models,
+                       maskw, opcap);
     const size_t smem = (size_t)lay.item_bytes * 4;
     if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v6 shared-memory footprint too large");
     if (smem > 48 * 1024)

@@ -68,8 +68,25 @@ static_assert(sizeof(V6Op) == 16, "V6Op layout");
 // Byte offsets of one item's shared-memory slice (host-computed).
 struct V6Layout {
     int item_bytes;
-    int rows, shard, aware, sw, tr, opval, opkey, key, cslot, rowdev;
+    int rows, shard, aware, sw, tr, opval, opmask, key, cslot, rowdev, mmask;
+    int ops_cap;  // op-buffer entries (multiple of 4, >= 32)
 };
+
+// Op buffer: a level's op list is compacted and walked in chunks of at most
+// `cap` entries (order preserved), so the shared-memory footprint does not
+// grow with the longest op template.  A small buffer leaves more of the SM's
+// unified L1/shared array to the L1 cache (the carve-out is sized by the
+// resident CTAs' shared memory).  Entry: 8-byte value + 8-byte device mask
+// (two device slots per lane, no overrides) or 4-byte key (otherwise).
+// Measured on B200 (config 5 / config 4): 64 entries for one device slot per
+// lane (the C5 slice drops to the 164 KB carve-out), 128 for two (fewer
+// chunk flushes on config 4's long templates outweigh the larger L1).
+template <int DPL>
+constexpr int v6_opcap_default() { return DPL == 1 ? 64 : 128; }
+inline int v6_ops_cap(int max_level_ops, int cap) {
+    const int ops4 = ((max_level_ops > 0 ? max_level_ops : 1) + 3) & ~3;
+    return ops4 < 32 ? 32 : (ops4 > cap ? cap : ops4);
+}
 
 // Static per-warp layouts for the common shapes: every field at a
 // compile-time offset from the warp's slice base, so the many shared-memory
@@ -96,10 +113,11 @@ struct V6Static {
 };
 
 template <int DPL>
-inline V6Layout v6_layout_static(int ops_cap) {
+inline V6Layout v6_layout_static(int max_level_ops, int n_models, bool maskw, int cap) {
     using S = typename V6Static<DPL>::T;
     V6Layout L{};
-    const int ops4 = ((ops_cap > 0 ? ops_cap : 1) + 3) & ~3;
+    const int ops4 = v6_ops_cap(max_level_ops, cap);
+    L.ops_cap = ops4;
     L.rows = (int)offsetof(S, rows);
     L.shard = (int)offsetof(S, shard);
     L.aware = (int)offsetof(S, aware);
@@ -109,12 +127,14 @@ inline V6Layout v6_layout_static(int ops_cap) {
     L.cslot = (int)offsetof(S, cslot);
     L.rowdev = (int)offsetof(S, rowdev);
     L.opval = (int)((sizeof(S) + 15) & ~size_t(15));
-    L.opkey = L.opval + 8 * ops4;
-    L.item_bytes = (L.opkey + 4 * ops4 + 15) & ~15;
+    L.opmask = L.opval + 8 * ops4;
+    L.mmask = L.opmask + (maskw ? 8 : 4) * ops4;
+    L.item_bytes = (L.mmask + (maskw ? 8 * n_models : 0) + 15) & ~15;
     return L;
 }
 
-inline V6Layout v6_layout(int D, int Bmax, int ops_cap) {
+inline V6Layout v6_layout(int D, int Bmax, int max_level_ops, int n_models, bool maskw,
+                          int cap) {
     V6Layout L{};
     int o = 0;
     const auto take = [&](int n, int sz) {
@@ -128,9 +148,11 @@ inline V6Layout v6_layout(int D, int Bmax, int ops_cap) {
     L.aware = take(V6_SLOTS, 8);
     L.sw = take(D, 8);
     L.tr = take(D, 8);
-    const int ops4 = ((ops_cap > 0 ? ops_cap : 1) + 3) & ~3;  // walked 4 at a time
+    const int ops4 = v6_ops_cap(max_level_ops, cap);  // walked 4 at a time
+    L.ops_cap = ops4;
     L.opval = take(ops4, 8);
-    L.opkey = take(ops4, 4);
+    L.opmask = take(ops4, maskw ? 8 : 4);
+    L.mmask = take(maskw ? n_models : 0, 8);
     L.key = take(D, 4);
     L.cslot = take(D, 4);
     L.rowdev = take(V6_RCAP, 4);
@@ -317,6 +339,32 @@ __device__ __forceinline__ void v6_apply(double (&aff)[DPL], double val, int k, 
     }
 }
 
+// Masked op of the non-override walk: the op applies to device t (t + 32)
+// iff bit t of lo (hi) is set -- one bit test per device slot, then the same
+// predicated add.rn.f64 as v6_apply.
+template <int DPL>
+__device__ __forceinline__ void v6_apply_m(double (&aff)[DPL], double val, unsigned lo,
+                                           unsigned hi, unsigned lanebit) {
+    if (DPL == 1) {
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 x;\n\t"
+            "and.b32 x, %2, %3;\n\t"
+            "setp.ne.b32 p, x, 0;\n\t"
+            "@p add.rn.f64 %0, %0, %1;\n\t}"
+            : "+d"(aff[0])
+            : "d"(val), "r"(lo), "r"(lanebit));
+    } else {
+        asm("{\n\t.reg .pred p, r;\n\t.reg .b32 x, y;\n\t"
+            "and.b32 x, %3, %5;\n\t"
+            "and.b32 y, %4, %5;\n\t"
+            "setp.ne.b32 p, x, 0;\n\t"
+            "setp.ne.b32 r, y, 0;\n\t"
+            "@p add.rn.f64 %0, %0, %2;\n\t"
+            "@r add.rn.f64 %1, %1, %2;\n\t}"
+            : "+d"(aff[0]), "+d"(aff[DPL - 1])
+            : "d"(val), "r"(lo), "r"(hi), "r"(lanebit));
+    }
+}
+
 // state.cached_tokens (state.py:110-123) for the stage group, with the first
 // two entries loaded speculatively next to the entry count (one dependent load
 // level less on the critical path; entries past the count are never used)
@@ -382,7 +430,9 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     double* const s_sw = SL ? ss->sw : reinterpret_cast<double*>(sb + lay.sw);
     double* const s_tr = SL ? ss->tr : reinterpret_cast<double*>(sb + lay.tr);
     double* const s_opval = reinterpret_cast<double*>(sb + lay.opval);
-    int* const s_opkey = reinterpret_cast<int*>(sb + lay.opkey);
+    uint2* const s_opmask = reinterpret_cast<uint2*>(sb + lay.opmask);
+    int* const s_opkey = reinterpret_cast<int*>(sb + lay.opmask);  // key walks: 4-byte keys
+    unsigned* const s_mm = reinterpret_cast<unsigned*>(sb + lay.mmask);
     int* const s_key = SL ? ss->key : reinterpret_cast<int*>(sb + lay.key);
     int* const s_cslot = SL ? ss->cslot : reinterpret_cast<int*>(sb + lay.cslot);
     int* const s_rowdev = SL ? ss->rowdev : reinterpret_cast<int*>(sb + lay.rowdev);
@@ -715,6 +765,21 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         for (int j = 0; j < DPL; ++j) tail[j] = tail_full[j];
     } else if (do_tail) {
         const V6Op* tmpl = reinterpret_cast<const V6Op*>(der.tmpl);
+        const unsigned lanebit = 1u << t;
+        // device masks per op for two device slots per lane; one slot keeps
+        // the op keys (three predicate ops per op, no per-item mask table)
+        constexpr bool MASKW = !OVR && DPL == 2;
+        if (MASKW) {
+            // s_mm[2x + j]: devices t + 32j whose displaced resident model is x
+            for (int i = t; i < 2 * b.n_models; i += 32) s_mm[i] = 0u;
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < DPL; ++j) {
+                const unsigned grp = __match_any_sync(FULL, dmc[j]);
+                if (dmc[j] >= 0) s_mm[2 * dmc[j] + j] = grp;
+            }
+            __syncwarp();
+        }
         #pragma unroll 1
         for (int l = 0; l < LV; ++l) {
             const long long vl = (long long)v * LV + l;
@@ -730,78 +795,127 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                 for (int j = 0; j < DPL; ++j) aff[j] = row[1 + dmc[j]];
             } else {
                 // op list from the level's template: static entries always, edge
-                // entries iff their parent is located (order preserved)
+                // entries iff their parent is located (order preserved), compacted
+                // and walked in chunks of at most lay.ops_cap entries.  Without
+                // overrides each entry carries the 64-bit mask of the devices it
+                // applies to (edge: all but the parent's location; displacement of
+                // model x: the devices whose displaced resident is x; otherwise
+                // all), so a device's predicate is one bit test.
                 const long long t0 = der.tmpl_ptr[vl], t1 = der.tmpl_ptr[vl + 1];
-                int base = 0;
-                #pragma unroll 1
-                for (long long j0 = t0; j0 < t1; j0 += 32) {
-                    const long long jx = j0 + t;
-                    bool keep = false;
-                    double val = 0.0;
-                    int key = 0;
-                    if (jx < t1) {
-                        const int4 raw = __ldg(reinterpret_cast<const int4*>(tmpl + jx));
-                        val = __hiloint2double(raw.y, raw.x);
-                        if (raw.z < 0) {
-                            keep = true;
-                            key = raw.w;
-                        } else {
-                            const int L = loc_row[raw.z];
-                            keep = L >= 0;
-                            key = OVR ? V6_KEY_SIGMA + L : L;
-                        }
-                    }
-                    const unsigned bal = __ballot_sync(FULL, keep);
-                    if (keep) {
-                        const int pos = base + __popc(bal & ((1u << t) - 1u));
-                        s_opval[pos] = val;
-                        s_opkey[pos] = key;
-                    }
-                    base += __popc(bal);
-                }
 #pragma unroll
                 for (int j = 0; j < DPL; ++j) aff[j] = 0.0;
-                if (!OVR) {
-                    // pad to a multiple of 4 with no-op entries; walk 4 ops per
-                    // iteration with one 16-byte key load and two 16-byte value loads
-                    const int nb4 = (base + 3) & ~3;
-                    if (t < nb4 - base) {
-                        s_opval[base + t] = 0.0;
-                        s_opkey[base + t] = V6_KEY_NOOP;
-                    }
-                    __syncwarp();
+                long long j0 = t0;
+                #pragma unroll 1
+                while (j0 < t1) {
+                    // compact template blocks until the buffer could overflow
+                    int base = 0;
                     #pragma unroll 1
-                    for (int o = 0; o < nb4; o += 4) {
-                        const int4 k4 = *reinterpret_cast<const int4*>(s_opkey + o);
-                        const double2 va = *reinterpret_cast<const double2*>(s_opval + o);
-                        const double2 vb = *reinterpret_cast<const double2*>(s_opval + o + 2);
-                        v6_apply<DPL>(aff, va.x, k4.x, dv, tgt);
-                        v6_apply<DPL>(aff, va.y, k4.y, dv, tgt);
-                        v6_apply<DPL>(aff, vb.x, k4.z, dv, tgt);
-                        v6_apply<DPL>(aff, vb.y, k4.w, dv, tgt);
-                    }
-                } else {
-                    __syncwarp();
-                    #pragma unroll 1
-                    for (int o = 0; o < base; ++o) {
-                        const int k = s_opkey[o];
-                        const double val = s_opval[o];
+                    do {
+                        const long long jx = j0 + t;
+                        bool keep = false;
+                        double val = 0.0;
+                        unsigned mlo = 0u, mhi = 0u;
+                        if (jx < t1) {
+                            const int4 raw = __ldg(reinterpret_cast<const int4*>(tmpl + jx));
+                            val = __hiloint2double(raw.y, raw.x);
+                            if (raw.z < 0) {
+                                keep = true;
+                                if (!MASKW) {
+                                    mlo = (unsigned)raw.w;
+                                } else if (raw.w == V6_KEY_ALWAYS) {
+                                    mlo = mhi = ~0u;
+                                } else {
+                                    const int mx = raw.w - V6_KEY_MODEL;
+                                    if (mx < b.n_models) {
+                                        mlo = s_mm[2 * mx];
+                                        mhi = s_mm[2 * mx + 1];
+                                    }
+                                }
+                            } else {
+                                const int L = loc_row[raw.z];
+                                keep = L >= 0;
+                                if (!MASKW) {
+                                    mlo = (unsigned)(OVR ? V6_KEY_SIGMA + L : L);
+                                } else {
+                                    mlo = L < 32 ? ~(1u << (L & 31)) : ~0u;
+                                    mhi = L >= 32 ? ~(1u << (L & 31)) : ~0u;
+                                }
+                            }
+                        }
+                        const unsigned bal = __ballot_sync(FULL, keep);
+                        if (keep) {
+                            const int pos = base + __popc(bal & ((1u << t) - 1u));
+                            s_opval[pos] = val;
+                            if (MASKW)
+                                s_opmask[pos] = make_uint2(mlo, mhi);
+                            else
+                                s_opkey[pos] = (int)mlo;
+                        }
+                        base += __popc(bal);
+                        j0 += 32;
+                    } while (j0 < t1 && base + 32 <= lay.ops_cap);
+                    // walk the buffered chunk
+                    if (MASKW) {
+                        // pad to a multiple of 4 with entries that match no device;
+                        // walk 4 ops per iteration (two 16-byte mask loads, two
+                        // 16-byte value loads)
+                        const int nb4 = (base + 3) & ~3;
+                        if (t < nb4 - base) {
+                            s_opval[base + t] = 0.0;
+                            s_opmask[base + t] = make_uint2(0u, 0u);
+                        }
+                        __syncwarp();
+                        #pragma unroll 1
+                        for (int o = 0; o < nb4; o += 4) {
+                            const uint4 ma = *reinterpret_cast<const uint4*>(s_opmask + o);
+                            const uint4 mb = *reinterpret_cast<const uint4*>(s_opmask + o + 2);
+                            const double2 va = *reinterpret_cast<const double2*>(s_opval + o);
+                            const double2 vb = *reinterpret_cast<const double2*>(s_opval + o + 2);
+                            v6_apply_m<DPL>(aff, va.x, ma.x, ma.y, lanebit);
+                            v6_apply_m<DPL>(aff, va.y, ma.z, ma.w, lanebit);
+                            v6_apply_m<DPL>(aff, vb.x, mb.x, mb.y, lanebit);
+                            v6_apply_m<DPL>(aff, vb.y, mb.z, mb.w, lanebit);
+                        }
+                    } else if (!OVR) {
+                        const int nb4 = (base + 3) & ~3;
+                        if (t < nb4 - base) {
+                            s_opval[base + t] = 0.0;
+                            s_opkey[base + t] = V6_KEY_NOOP;
+                        }
+                        __syncwarp();
+                        #pragma unroll 1
+                        for (int o = 0; o < nb4; o += 4) {
+                            const int4 k4 = *reinterpret_cast<const int4*>(s_opkey + o);
+                            const double2 va = *reinterpret_cast<const double2*>(s_opval + o);
+                            const double2 vb = *reinterpret_cast<const double2*>(s_opval + o + 2);
+                            v6_apply<DPL>(aff, va.x, k4.x, dv, tgt);
+                            v6_apply<DPL>(aff, va.y, k4.y, dv, tgt);
+                            v6_apply<DPL>(aff, vb.x, k4.z, dv, tgt);
+                            v6_apply<DPL>(aff, vb.y, k4.w, dv, tgt);
+                        }
+                    } else {
+                        __syncwarp();
+                        #pragma unroll 1
+                        for (int o = 0; o < base; ++o) {
+                            const int k = s_opkey[o];
+                            const double val = s_opval[o];
 #pragma unroll
-                        for (int j = 0; j < DPL; ++j) {
-                            if (k < V6_KEY_MODEL) {
-                                if (k != dv[j]) aff[j] += val;
-                            } else if (k < V6_KEY_SIGMA) {
-                                if (k - V6_KEY_MODEL == dmc[j]) aff[j] += val;
-                            } else if (k - V6_KEY_SIGMA != dv[j]) {
-                                aff[j] -= w.lambda_tr *
-                                          b.beta[(size_t)(k - V6_KEY_SIGMA) * D +
-                                                 (live[j] ? dv[j] : 0)] *
-                                          val * w.transfer_x * w.locality_scale;
+                            for (int j = 0; j < DPL; ++j) {
+                                if (k < V6_KEY_MODEL) {
+                                    if (k != dv[j]) aff[j] += val;
+                                } else if (k < V6_KEY_SIGMA) {
+                                    if (k - V6_KEY_MODEL == dmc[j]) aff[j] += val;
+                                } else if (k - V6_KEY_SIGMA != dv[j]) {
+                                    aff[j] -= w.lambda_tr *
+                                              b.beta[(size_t)(k - V6_KEY_SIGMA) * D +
+                                                     (live[j] ? dv[j] : 0)] *
+                                              val * w.transfer_x * w.locality_scale;
+                                }
                             }
                         }
                     }
+                    __syncwarp();  // op buffer reused by the next chunk / level
                 }
-                __syncwarp();  // op buffer reused by the next level
             }
 #pragma unroll
             for (int j = 0; j < DPL; ++j)

@@ -280,8 +280,8 @@ class DeviceBank:
                 torch.cumsum(counts, 0, out=self.tmpl_ptr[1:])
         n_tmpl = int(self.tmpl_ptr[-1].item()) if nvl else 0
         if nvl:
-            # the longest op template bounds every level's op list (the kernels'
-            # op buffers); tighter than the window-based max_level_ops
+            # the longest op template bounds every level's op list; the v6
+            # kernel sizes its (chunked) op buffer by min(this, its cap)
             longest = int((self.tmpl_ptr[1:] - self.tmpl_ptr[:-1]).max().item())
             self.cwin.max_level_ops = min(self.cwin.max_level_ops, max(longest, 1))
         self.tmpl = torch.empty(max(n_tmpl, 1) * 16, dtype=torch.uint8, device=self.device)
