@@ -92,6 +92,31 @@ def test_c4_frontier_and_sweep_sample():
     assert_parity(c4_case(scen=(0, 3), sweep_stride=97))
 
 
+def test_smallest_op_buffer_chunks_every_long_level():
+    """Op lists walked in 32-entry chunks (FATE_V6_OPCAP=32, read once per
+    process, hence the subprocess) stay bit-identical: transfer overrides,
+    one and two device slots per lane, config-4 templates of several hundred
+    ops."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import test_gpu_parity as T\n"
+        "from cases import c4_case, c5_case, edge_case\n"
+        "for h in (2, 4, 6): T.assert_parity(edge_case(horizon=h))\n"
+        "T.assert_parity(edge_case(horizon=4, overrides=False))\n"
+        "T.assert_parity(c5_case(n_inst=3))\n"
+        "T.assert_parity(c4_case(scen=(1,), sweep_stride=211))\n"
+        "print('ok')\n" % (here, os.path.dirname(here)))
+    env = dict(os.environ, FATE_V6_OPCAP="32")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
 def test_library_is_native():
     """The scorer ran from the in-tree libfate.so, and launched kernels."""
     before = runtime.launch_count()
