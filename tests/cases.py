@@ -238,3 +238,97 @@ def token_case(seed: int = 3, horizon: int = 3):
 
 
 ALL_ABLATIONS = ("no_future_planning", "no_locality", "no_same_model", "no_prefix", "no_shard")
+
+
+def wide_case(n_dev: int, n_queries: int, kappa: int, overrides: bool, horizon: int = 4,
+              seed: int = 11, n_stages: int = 30, uniform_speed: bool = False,
+              n_scen: int = 3):
+    """Random layered DAG at the ABI's size limits: up to 64 devices (one or
+    two device slots per lane, the 32/33 boundary), query batches past the
+    static 16-query layout up to MAX_QUERIES, up to MAX_KAPPA prefix entries
+    per device, eight models (displacement masks), transfer overrides on or
+    off, shard bounds 1-4, restricted and empty eligibility."""
+    rng = random.Random(seed)
+    cat = scenarios.config_c4_catalog()
+    models = cat.models
+    aliases = sorted(models)
+    roles = list(cat.roles.values())
+    devs = [DeviceSpec(id=f"w{i:02d}", speed_factor=1.0 if uniform_speed else
+                       rng.choice([0.5, 0.8, 1.0, 1.25, 2.0])) for i in range(n_dev)]
+    dev_ids = [d.id for d in devs]
+    over = {}
+    if overrides:
+        for a in dev_ids:
+            for b in rng.sample(dev_ids, min(3, n_dev)):
+                if a != b:
+                    over[(a, b)] = rng.choice([0.5, 1.5, 3.0, 0.0])
+    topo = DeviceTopology(devices=tuple(devs), default_transfer_coeff=2.0,
+                          transfer_overrides=over)
+    ids = [f"s{i:03d}" for i in range(n_stages)]
+    width = 5
+    levels = [ids[i:i + width] for i in range(0, n_stages, width)]
+    edges = set()
+    for li in range(1, len(levels)):
+        for v in levels[li]:
+            ups = [u for u in levels[li - 1] if rng.random() < 0.5] or [levels[li - 1][0]]
+            edges.update((u, v) for u in ups)
+            if li >= 2 and rng.random() < 0.4:
+                edges.add((rng.choice(levels[li - 2]), v))
+    groups = ["pg0", "pg1", "pg2", None]
+    stages = {}
+    for i, sid in enumerate(ids):
+        role = None if i % 11 == 5 else roles[i % len(roles)]
+        if i % 7 == 3:
+            elig = frozenset(rng.sample(dev_ids, max(1, n_dev // 2)))
+        else:
+            elig = frozenset(dev_ids)
+        if i == n_stages - 2:
+            elig = frozenset()
+        shard = 1 if (role is not None and not role.shard_eligible) else 1 + i % 4
+        stages[sid] = Stage(id=sid, model=None if i % 13 == 6 else aliases[i % len(aliases)],
+                            eligible_devices=elig, shard_bound=shard, role=role,
+                            prompt_token_proxy=rng.choice([0, 256, 512, 768, 1024]),
+                            output_token_proxy=rng.choice([0, 128, 384, 640]),
+                            shared_prefix_group=groups[i % 4], keep_cache=bool(i % 2),
+                            cache_reuse=bool(i % 3))
+    dag = annotate_topology(WorkflowDag("wide", "wide", stages, frozenset(edges)))
+    qgroups = ["qa", "qb", "pg1", None]
+    queries = tuple(Query(f"q{i:03d}", 50 + rng.randrange(950), qgroups[i % 4])
+                    for i in range(n_queries))
+    inst = WorkflowInstance(dag=dag, queries=queries, batch_size=n_queries,
+                            prefix_groups={"qa": 100, "qb": 700})
+    weights = replace(ScoreWeights(), horizon=horizon, switch_x=1.25, transfer_x=0.5,
+                      prefix_x=1.5, state_scale=0.75, locality_scale=1.5)
+    kgroups = ["pg0", "pg1", "pg2", "qa", "qb"] + [f"x{k}" for k in range(max(0, kappa - 5))]
+    states = []
+    for s in range(n_scen):
+        st = ExecutionState.initial(inst, topo.device_ids)
+        st.clock = 10.0 + 40.0 * s
+        r2 = random.Random(seed * 100 + s)
+        for sid in sorted(ids)[: width * (s + 1)]:
+            d1, d2 = r2.sample(dev_ids, 2) if n_dev > 1 else (dev_ids[0], dev_ids[0])
+            qids = tuple(q.query_id for q in queries)
+            if n_dev > 1 and r2.random() < 0.3 and len(qids) > 1:
+                h = len(qids) // 2
+                st.parent_loc[sid] = ((d1, qids[:h]), (d2, qids[h:]))
+            else:
+                st.parent_loc[sid] = ((d1, qids),)
+            st.completed.add(sid)
+        for d in dev_ids:
+            st.residency[d] = r2.choice([None] + aliases)
+            st.device_free[d] = st.clock + r2.choice([-5.0, 0.0, 1e-13, 3.0, 12.5])
+            store = st.prefix_store[d]
+            for g in r2.sample(kgroups, r2.randint(0, kappa)) if d != dev_ids[0] else kgroups[:kappa]:
+                store[g] = PrefixEntry(g, r2.choice([30, 256, 400, 5000]),
+                                       r2.choice(aliases + [""]), sticky=r2.random() < 0.5)
+        states.append((0, st))
+    bank_tmp = pack.pack_bank([inst], models, topo)
+    items = [(j, bank_tmp.global_index(0, sid)) for j in range(len(states)) for sid in ids]
+
+    class _Cfg:
+        pass
+
+    c = _Cfg()
+    c.models, c.topology = models, topo
+    return Case(f"wide-d{n_dev}-b{n_queries}-k{kappa}-o{int(overrides)}-h{horizon}", [inst], c,
+                weights, states, items)

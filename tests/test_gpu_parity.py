@@ -9,6 +9,8 @@ empty-model prefix entries, idle and busy devices), every ablation, horizons
 
 from __future__ import annotations
 
+from dataclasses import replace
+
 import numpy as np
 import pytest
 
@@ -16,7 +18,8 @@ import oracle
 from paper_2605_07238_b200 import pack, runtime
 from paper_2605_07238_b200.wf.weights import AblationFlags
 
-from cases import ALL_ABLATIONS, bits, c4_case, c5_case, edge_case, small_case, token_case
+from cases import (ALL_ABLATIONS, bits, c4_case, c5_case, edge_case, small_case, token_case,
+                   wide_case)
 
 pytestmark = pytest.mark.gpu
 
@@ -105,8 +108,9 @@ def test_smallest_op_buffer_chunks_every_long_level():
     code = (
         "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
         "import test_gpu_parity as T\n"
-        "from cases import c4_case, c5_case, edge_case\n"
+        "from cases import c4_case, c5_case, edge_case, wide_case\n"
         "for h in (2, 4, 6): T.assert_parity(edge_case(horizon=h))\n"
+        "for a in T.WIDE[:4]: T.assert_parity(wide_case(*a))\n"
         "T.assert_parity(edge_case(horizon=4, overrides=False))\n"
         "T.assert_parity(c5_case(n_inst=3))\n"
         "T.assert_parity(c4_case(scen=(1,), sweep_stride=211))\n"
@@ -115,6 +119,43 @@ def test_smallest_op_buffer_chunks_every_long_level():
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+WIDE = [
+    (64, 40, 6, True, 4),     # two device slots, overrides, runtime layout (B > 16)
+    (64, 16, 2, False, 4),    # two device slots, device-mask walk, static layout
+    (33, 16, 3, False, 3),    # first two-slot size: one live device in slot 1
+    (32, 256, 12, True, 5),   # last one-slot size, MAX_QUERIES queries
+    (48, 24, 4, False, 6),    # two slots, runtime layout, horizon 6
+    (8, 16, 64, True, 4),     # MAX_KAPPA prefix entries on a device
+    (1, 1, 1, False, 2),      # one device, one query
+]
+
+
+@pytest.mark.parametrize("args", WIDE, ids=lambda a: "d%d-b%d-k%d-o%d-h%d" % a)
+def test_wide_shapes(args):
+    assert_parity(wide_case(*args))
+
+
+def test_wide_shapes_uniform_speed_ablations():
+    for flag in ALL_ABLATIONS:
+        case = wide_case(64, 16, 3, False, 4, seed=5, uniform_speed=True)
+        case.weights = replace(case.weights, ablation=AblationFlags.from_names([flag]))
+        case.wrec = pack.weights_record(case.weights)
+        case.work = pack.make_work(case.bank, [(int(s), int(g)) for s, g in
+                                               zip(case.work.scen, case.work.stage)],
+                                   case.weights.ablation.no_shard)
+        assert_parity(case)
+
+
+def test_empty_work_list_is_a_no_op():
+    case = edge_case(horizon=3)
+    dbank = runtime.DeviceBank(case.bank, case.weights)
+    empty = pack.make_work(case.bank, [], False)
+    before = runtime.launch_count()
+    res = dbank.score(case.states, empty, extras=True)
+    assert res.psi.numel() >= 0 and empty.n_psi == 0
+    assert runtime.launch_count() == before
 
 
 def test_library_is_native():
