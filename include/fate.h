@@ -372,7 +372,8 @@ typedef struct fate_host_batch {
     int32_t n_items;
     int32_t reserved;
     int64_t n_psi;                  /* entries of the Psi output */
-    const fate_item* items;         /* [n_items], scenario-major, psi_off increasing */
+    const fate_item* items;         /* [n_items], scenario-major, psi_off non-decreasing
+                                       (equal for an item without candidates) */
 } fate_host_batch;
 
 /* Opaque per-(process, GPU) handle: its streams, events and device

@@ -189,13 +189,18 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
         unsigned bad = (unsigned)it[0].scen >= (unsigned)S;
         for (int i = 1; i < W; ++i)
             bad |= ((unsigned)it[i].scen >= (unsigned)S) | (it[i].scen < it[i - 1].scen) |
-                   (it[i].psi_off <= it[i - 1].psi_off);
+                   (it[i].psi_off < it[i - 1].psi_off);
         if (bad)
             return fate_internal_fail(FATE_EINVAL,
                                       "fate_pipeline_score: items must be scenario-major (scenario "
-                                      "in range), psi_off increasing");
+                                      "in range), psi_off non-decreasing");
     }
-    if (it[0].psi_off < 0 || it[W - 1].psi_off >= hb->n_psi)
+    // psi_off == n_psi is a trailing item without candidates (no eligible
+    // device); the device Psi workspace carries 64 * D slack entries past
+    // n_psi, so even an item whose bound the host cannot see (the bank is
+    // device-resident) never writes outside the workspace -- only [0, n_psi)
+    // is copied back
+    if (it[0].psi_off < 0 || it[W - 1].psi_off > hb->n_psi)
         return fate_internal_fail(FATE_EINVAL, "fate_pipeline_score: psi_off out of range");
     const auto loc_off = [&](int s) -> int64_t {
         int64_t v;
@@ -221,7 +226,7 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
         (rc = grow(p, p->dev_free, 8 * (size_t)S * D)) || (rc = grow(p, p->kappa_n, 4 * (size_t)S * D)) ||
         (rc = grow(p, p->kappa, 16 * (size_t)S * D * cap)) || (rc = grow(p, p->w_scen, 4 * (size_t)W)) ||
         (rc = grow(p, p->w_stage, 4 * (size_t)W)) || (rc = grow(p, p->w_psi_off, 8 * (size_t)W)) ||
-        (rc = grow(p, p->psi, 8 * (size_t)hb->n_psi)))
+        (rc = grow(p, p->psi, 8 * ((size_t)hb->n_psi + 64 * (size_t)D))))
         return rc;
     if (sched_host && (rc = grow(p, p->sched, 8 * (size_t)W * D))) return rc;
     if (completion_host && (rc = grow(p, p->completion, 8 * (size_t)W * D))) return rc;

@@ -196,6 +196,28 @@ def test_host_pipeline_chunks_match_device_path():
     assert np.array_equal(bits(got.numpy()[:n]), bits(want))
 
 
+@pytest.mark.parametrize("args", [WIDE[0], WIDE[3], WIDE[5]],
+                         ids=lambda a: "d%d-b%d-k%d-o%d-h%d" % a)
+def test_host_pipeline_wide_shapes_match_oracle(args):
+    """Host wire records at their largest (64 devices x 6 entries, 64
+    entries per device, 256 queries) through the pipeline equal the oracle."""
+    import torch
+
+    case = wide_case(*args)
+    dbank = runtime.DeviceBank(case.bank, case.weights)
+    pipe = runtime.HostPipeline(dbank, case.states, case.work, extras=True, n_chunks=2,
+                                graph=True)
+    got = pipe.run()
+    torch.cuda.synchronize()
+    want = oracle.score(case.bank, case.wrec, case.states, case.work)
+    n = case.work.n_psi
+    m = case.work.n_items * case.bank.scalars["n_devices"]
+    assert np.array_equal(bits(got.numpy()[:n]), bits(want["psi"]))
+    assert np.array_equal(bits(pipe.host_sched.numpy()[:m]), bits(want["sched"]))
+    assert np.array_equal(bits(pipe.host_completion.numpy()[:m]), bits(want["completion"]))
+    pipe.close()
+
+
 def test_host_pipeline_graph_replays_fresh_inputs():
     """A captured pipeline re-reads the pinned inputs on every replay."""
     import torch
