@@ -265,9 +265,21 @@ def issue_ceiling(key: str, ms: float, sm_mhz) -> dict | None:
         return None
     peak = 148 * 4 * float(sm_mhz) * 1e6
     achieved = inst / (ms / 1e3)
-    return {"bound": "issue", "warp_instructions_per_launch": inst,
-            "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "G warp-inst/s",
-            "frac": achieved / peak, "source": "profiles/ncu_instructions.json"}
+    out = {"bound": "issue", "warp_instructions_per_launch": inst,
+           "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "G warp-inst/s",
+           "frac": achieved / peak, "source": "profiles/ncu_instructions.json"}
+    # single-pipe ceilings measured by tools/issue_probe.cu on this pool's B200
+    # (the integer ALU and FP64 pipes each retire a warp instruction every
+    # other cycle per scheduler; a mixed stream is needed to pass ~52 %)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_issue_probe.json")) as fh:
+            probe = json.load(fh)
+        out["measured_pipes"] = {k: probe[k] for k in
+                                 ("int_issue_ginst_s", "dadd_ginst_s", "walk_warp_ops_g_per_s")}
+        out["measured_pipes"]["source"] = "profiles/r01_issue_probe.json"
+    except Exception:
+        pass
+    return out
 
 
 def time_device(torch, dbank, dstates, dwork, out, steps, warmup, flush, world, device,
