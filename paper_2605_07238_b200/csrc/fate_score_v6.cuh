@@ -23,11 +23,19 @@
 //    level's op list is built with one coalesced 16-byte load and one loc
 //    gather per 32 entries plus a ballot compaction, no nested parent loops;
 //  * op walk with predicated adds (inline PTX: two predicate-combining setp
-//    and one predicated add.rn.f64 per device slot).  Skipping an op equals
-//    adding +0.0 exactly because the chain starts at +0.0 and never becomes
-//    -0.0 in round-to-nearest (v5's argument), so this is v5's chain bit for
-//    bit;
-//  * shared-memory layout offsets computed once on the host (V6Layout).
+//    and one predicated add.rn.f64 per device slot; with two device slots per
+//    lane and no overrides each buffered op carries the 64-bit mask of the
+//    devices it applies to, so the predicate is one bit test).  Skipping an
+//    op equals adding +0.0 exactly because the chain starts at +0.0 and never
+//    becomes -0.0 in round-to-nearest (v5's argument), so this is v5's chain
+//    bit for bit;
+//  * op lists compacted and walked in chunks through a small per-warp buffer
+//    (order preserved), so shared memory does not grow with the longest
+//    template and the L1 carve-out stays large;
+//  * shared-memory layout offsets computed once on the host (V6Layout); the
+//    warp's slice base comes from a lane-0 shuffle (a uniform register) and
+//    the lane id from %laneid, so neither is rematerialised from threadIdx
+//    under the register budget.
 
 constexpr int V6_KT = 4;               // shard counts k <= V6_KT: shard sums tabulated
 constexpr int V6_RCAP = 8;             // dynamic classes with a shared-memory row
