@@ -336,9 +336,10 @@ int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_window
     const char* e = getenv("FATE_MINB");
     // register budget (CTAs per SM), measured on B200: 10 for one device slot
     // per lane (48 registers: the extra warps hide more latency than the
-    // spills cost; 8/9/12 were slower), 7 for two (72 registers).  FATE_MINB
-    // = 7 | 8 | 10 selects another instantiation (A/B only).
-    switch (e ? atoi(e) : (DPL == 1 ? 10 : 7)) {
+    // spills cost; 8/9/12 were slower), 8 for two (64 registers; 1 % ahead of
+    // 7 x 72 registers once the chunked op buffer let 8 CTAs fit in shared
+    // memory).  FATE_MINB = 7 | 8 | 10 selects another instantiation (A/B).
+    switch (e ? atoi(e) : (DPL == 1 ? 10 : 8)) {
         case 7:
             return ovr ? launch_v6_mb<DPL, true, SL, 7>(bank, w, win, der, st, work, out, s)
                        : launch_v6_mb<DPL, false, SL, 7>(bank, w, win, der, st, work, out, s);
