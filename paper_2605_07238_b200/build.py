@@ -4,7 +4,7 @@
 ``--fmad=false`` is part of the exactness contract: it forbids contracting
 ``a*b+c`` into ``fma.rn.f64``, which would change Psi bits relative to
 CPython.  After building, the PTX is scanned and the build fails if any
-``fma.rn.f64`` survived.
+``fma.rn.f64`` survived outside the walk's tagged exact 0/1-factor blocks.
 """
 
 from __future__ import annotations
@@ -48,10 +48,20 @@ def check_ptx(verbose: bool = False) -> str:
     ptx = os.path.join(HERE, "fate_kernels.ptx")
     cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-ptx", SOURCES[0], "-o", ptx]
     subprocess.run(cmd, check=True, capture_output=not verbose)
-    text = open(ptx).read()
-    if re.search(r"\bfma\.rn\.f64\b", text):
+    if not ptx_contraction_free(open(ptx).read()):
         raise RuntimeError("fma.rn.f64 found in PTX: exactness contract broken")
     return ptx
+
+
+def ptx_contraction_free(text: str) -> bool:
+    """True iff every ``fma.rn.f64`` in the PTX is one of the walk's exact
+    0/1-factor FMAs, emitted from inline asm blocks tagged ``fate-fma01``
+    (fma(v, 1, a) == v + a and fma(v, 0, a) == a bit for bit); any other is
+    a contracted a*b+c."""
+    blocks = re.split(r"(// begin inline asm.*?// end inline asm)", text, flags=re.S)
+    rest = "".join(b for b in blocks
+                   if not (b.startswith("// begin inline asm") and "fate-fma01" in b))
+    return re.search(r"\bfma\.rn\.f64\b", rest) is None
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -326,11 +326,14 @@ template <int DPL>
 __device__ __forceinline__ void v6_apply(double (&aff)[DPL], double val, int k, const int (&d)[DPL],
                                          const int (&tgt)[DPL]) {
     if (DPL == 1) {
-        asm("{\n\t.reg .pred q, p;\n\t"
+        // 0/1-factor FMA form (see v6_apply_m): same bits as the predicated add
+        asm("{\n\t// fate-fma01\n\t.reg .pred q, p;\n\t.reg .b32 h;\n\t.reg .f64 f;\n\t"
             "setp.lt.s32 q, %2, 1000;\n\t"
             "setp.ne.and.s32 p, %2, %3, q;\n\t"
             "setp.eq.or.s32 p, %2, %4, p;\n\t"
-            "@p add.rn.f64 %0, %0, %1;\n\t}"
+            "selp.b32 h, 0x3ff00000, 0, p;\n\t"
+            "mov.b64 f, {0, h};\n\t"
+            "fma.rn.f64 %0, %1, f, %0;\n\t}"
             : "+d"(aff[0])
             : "d"(val), "r"(k), "r"(d[0]), "r"(tgt[0]));
     } else {
@@ -361,13 +364,25 @@ __device__ __forceinline__ void v6_apply_m(double (&aff)[DPL], double val, unsig
             : "+d"(aff[0])
             : "d"(val), "r"(lo), "r"(lanebit));
     } else {
-        asm("{\n\t.reg .pred p, r;\n\t.reg .b32 x, y;\n\t"
+        // 0/1 factor form: aff = fma(val, f, aff) with f = +1.0 or +0.0 selected
+        // on its high word.  fma(v, 1, a) = RN(v + a) is the add itself and
+        // fma(v, 0, a) = RN(+-0 + a) = a since the chain is never -0.0 -- the
+        // same bits as the predicated add, with one select instead of the two
+        // ptxas emits to if-convert it (B200: 95 vs 80 G warp-ops/s,
+        // tools/issue_probe.cu).  The marker lets build.py's contraction
+        // check tell this exact FMA from a contracted a*b+c.
+        asm("{\n\t// fate-fma01\n\t.reg .pred p, r;\n\t.reg .b32 x, y, hx, hy;\n\t"
+            ".reg .f64 f, g;\n\t"
             "and.b32 x, %3, %5;\n\t"
             "and.b32 y, %4, %5;\n\t"
             "setp.ne.b32 p, x, 0;\n\t"
             "setp.ne.b32 r, y, 0;\n\t"
-            "@p add.rn.f64 %0, %0, %2;\n\t"
-            "@r add.rn.f64 %1, %1, %2;\n\t}"
+            "selp.b32 hx, 0x3ff00000, 0, p;\n\t"
+            "selp.b32 hy, 0x3ff00000, 0, r;\n\t"
+            "mov.b64 f, {0, hx};\n\t"
+            "mov.b64 g, {0, hy};\n\t"
+            "fma.rn.f64 %0, %2, f, %0;\n\t"
+            "fma.rn.f64 %1, %2, g, %1;\n\t}"
             : "+d"(aff[0]), "+d"(aff[DPL - 1])
             : "d"(val), "r"(lo), "r"(hi), "r"(lanebit));
     }

@@ -208,3 +208,19 @@ def test_host_batch_wire_format_round_trip():
     assert hb.items.itemsize == 16
     assert np.array_equal(hb.items["stage"], case.work.stage)
     assert np.array_equal(hb.items["psi_off"], case.work.psi_off)
+
+
+def test_ptx_contraction_check_allows_only_tagged_exact_fmas():
+    from paper_2605_07238_b200 import build
+
+    tagged = ("// begin inline asm\n{\n\t// fate-fma01\n\tfma.rn.f64 %fd1, %fd2, f, %fd1;\n}\n"
+              "// end inline asm\n")
+    plain = "\tfma.rn.f64 %fd3, %fd4, %fd5, %fd6;\n"
+    untagged_asm = "// begin inline asm\n\tfma.rn.f64 %fd1, %fd2, %fd3, %fd1;\n// end inline asm\n"
+    assert build.ptx_contraction_free("add.rn.f64 %fd1, %fd2, %fd3;\n" + tagged)
+    assert not build.ptx_contraction_free(tagged + plain)
+    assert not build.ptx_contraction_free(untagged_asm)
+    built = os.path.join(ROOT, "paper_2605_07238_b200", "fate_kernels.ptx")
+    if os.path.exists(built):  # by-product of build(); the build itself also checks
+        with open(built) as fh:
+            assert build.ptx_contraction_free(fh.read())

@@ -69,6 +69,7 @@ __global__ void k_dadd(double* out, double v) {
 // the v6 device-mask walk loop for two device slots: 4 ops per iteration,
 // masks and values from shared memory (two 16-byte mask loads, two 16-byte
 // value loads), exactly the production loop's shape
+template <int MODE>
 __global__ void k_walk(double* out, const uint2* gmask, const double* gval) {
     __shared__ __align__(16) uint2 sm[4][64];
     __shared__ __align__(16) double sv[4][64];
@@ -90,16 +91,44 @@ __global__ void k_walk(double* out, const uint2* gmask, const double* gval) {
         const unsigned ml[4] = {ma.x, ma.z, mb.x, mb.z}, mh[4] = {ma.y, ma.w, mb.y, mb.w};
         const double vv[4] = {va.x, va.y, vb.x, vb.y};
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-            asm("{\n\t.reg .pred p, q;\n\t.reg .b32 x, y;\n\t"
-                "and.b32 x, %2, %4;\n\t"
-                "and.b32 y, %3, %4;\n\t"
-                "setp.ne.b32 p, x, 0;\n\t"
-                "setp.ne.b32 q, y, 0;\n\t"
-                "@p add.rn.f64 %0, %0, %5;\n\t"
-                "@q add.rn.f64 %1, %1, %5;\n\t}"
-                : "+d"(a0), "+d"(a1)
-                : "r"(ml[r]), "r"(mh[r]), "r"(lb), "d"(vv[r]));
+        for (int r = 0; r < 4; ++r) {
+            if (MODE == 0)  // production: predicated add (ptxas: DADD + FSEL pair)
+                asm("{\n\t.reg .pred p, q;\n\t.reg .b32 x, y;\n\t"
+                    "and.b32 x, %2, %4;\n\t"
+                    "and.b32 y, %3, %4;\n\t"
+                    "setp.ne.b32 p, x, 0;\n\t"
+                    "setp.ne.b32 q, y, 0;\n\t"
+                    "@p add.rn.f64 %0, %0, %5;\n\t"
+                    "@q add.rn.f64 %1, %1, %5;\n\t}"
+                    : "+d"(a0), "+d"(a1)
+                    : "r"(ml[r]), "r"(mh[r]), "r"(lb), "d"(vv[r]));
+            else if (MODE == 1)  // 0/1 factor: select the high word of 1.0, one DFMA
+                asm("{\n\t.reg .pred p, q;\n\t.reg .b32 x, y, hx, hy;\n\t.reg .f64 f, g;\n\t"
+                    "and.b32 x, %2, %4;\n\t"
+                    "and.b32 y, %3, %4;\n\t"
+                    "setp.ne.b32 p, x, 0;\n\t"
+                    "setp.ne.b32 q, y, 0;\n\t"
+                    "selp.b32 hx, 0x3ff00000, 0, p;\n\t"
+                    "selp.b32 hy, 0x3ff00000, 0, q;\n\t"
+                    "mov.b64 f, {0, hx};\n\t"
+                    "mov.b64 g, {0, hy};\n\t"
+                    "fma.rn.f64 %0, %5, f, %0;\n\t"
+                    "fma.rn.f64 %1, %5, g, %1;\n\t}"
+                    : "+d"(a0), "+d"(a1)
+                    : "r"(ml[r]), "r"(mh[r]), "r"(lb), "d"(vv[r]));
+            else  // select the addend (value or +0.0), then add
+                asm("{\n\t.reg .pred p, q;\n\t.reg .b32 x, y;\n\t.reg .f64 u, w;\n\t"
+                    "and.b32 x, %2, %4;\n\t"
+                    "and.b32 y, %3, %4;\n\t"
+                    "setp.ne.b32 p, x, 0;\n\t"
+                    "setp.ne.b32 q, y, 0;\n\t"
+                    "selp.f64 u, %5, 0d0000000000000000, p;\n\t"
+                    "selp.f64 w, %5, 0d0000000000000000, q;\n\t"
+                    "add.rn.f64 %0, %0, u;\n\t"
+                    "add.rn.f64 %1, %1, w;\n\t}"
+                    : "+d"(a0), "+d"(a1)
+                    : "r"(ml[r]), "r"(mh[r]), "r"(lb), "d"(vv[r]));
+        }
     }
     out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1;
 }
@@ -148,7 +177,11 @@ int main() {
         cudaMemcpy(gmask, hm, sizeof(hm), cudaMemcpyHostToDevice);
         cudaMemcpy(gval, hv, sizeof(hv), cudaMemcpyHostToDevice);
     }
-    const double s_walk = time([&] { k_walk<<<blocks, threads>>>((double*)buf, gmask, gval); });
+    const double s_walk = time([&] { k_walk<0><<<blocks, threads>>>((double*)buf, gmask, gval); });
+    const double s_walk_fma =
+        time([&] { k_walk<1><<<blocks, threads>>>((double*)buf, gmask, gval); });
+    const double s_walk_sel =
+        time([&] { k_walk<2><<<blocks, threads>>>((double*)buf, gmask, gval); });
     const double it = (double)ITERS;
     const double int_inst = warps * it * (32 + 3);
     const double dadd_inst = warps * it * 32;
@@ -157,10 +190,12 @@ int main() {
     printf("{\"sms\": %d, \"clock_mhz_attr\": %.0f, "
            "\"issue_peak_ginst_s_at_attr_clock\": %.2f, "
            "\"int_issue_ginst_s\": %.2f, \"dadd_ginst_s\": %.2f, \"dadd_gflops\": %.1f, "
-           "\"walk_warp_ops_g_per_s\": %.2f, "
+           "\"walk_warp_ops_g_per_s\": %.2f, \"walk_fma01_warp_ops_g_per_s\": %.2f, "
+           "\"walk_seladd_warp_ops_g_per_s\": %.2f, "
            "\"seconds\": {\"int\": %.6f, \"dadd\": %.6f, \"walk\": %.6f}}\n",
            sms, clk_khz / 1e3, peak_issue / 1e9, int_inst / s_int / 1e9, dadd_inst / s_dadd / 1e9,
-           dadd_inst * 32 / s_dadd / 1e9, walk_ops / s_walk / 1e9, s_int, s_dadd, s_walk);
+           dadd_inst * 32 / s_dadd / 1e9, walk_ops / s_walk / 1e9, walk_ops / s_walk_fma / 1e9,
+           walk_ops / s_walk_sel / 1e9, s_int, s_dadd, s_walk);
     cudaFree(buf);
     return 0;
 }
