@@ -275,7 +275,8 @@ def issue_ceiling(key: str, ms: float, sm_mhz) -> dict | None:
         with open(os.path.join(ROOT, "profiles", "r01_issue_probe.json")) as fh:
             probe = json.load(fh)
         out["measured_pipes"] = {k: probe[k] for k in
-                                 ("int_issue_ginst_s", "dadd_ginst_s", "walk_warp_ops_g_per_s")}
+                                 ("int_issue_ginst_s", "dadd_ginst_s",
+                                  "walk_fma01_warp_ops_g_per_s") if k in probe}
         out["measured_pipes"]["source"] = "profiles/r01_issue_probe.json"
     except Exception:
         pass
