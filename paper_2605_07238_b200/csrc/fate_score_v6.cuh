@@ -86,11 +86,12 @@ struct V6Layout {
 // unified L1/shared array to the L1 cache (the carve-out is sized by the
 // resident CTAs' shared memory).  Entry: 8-byte value + 8-byte device mask
 // (two device slots per lane, no overrides) or 4-byte key (otherwise).
-// Measured on B200 (config 5 / config 4): 64 entries for one device slot per
-// lane (the C5 slice drops to the 164 KB carve-out), 128 for two (fewer
-// chunk flushes on config 4's long templates outweigh the larger L1).
+// Measured on B200: 64 entries (config 5: the resident slices fit the
+// 164 KB carve-out, 2 % faster than 128 entries; config 4 at 8 CTAs per SM:
+// 1.5 % faster than 96 or 128 entries -- the larger L1 outweighs the extra
+// chunk flushes on its long templates).
 template <int DPL>
-constexpr int v6_opcap_default() { return DPL == 1 ? 64 : 128; }
+constexpr int v6_opcap_default() { return 64; }
 inline int v6_ops_cap(int max_level_ops, int cap) {
     const int ops4 = ((max_level_ops > 0 ? max_level_ops : 1) + 3) & ~3;
     return ops4 < 32 ? 32 : (ops4 > cap ? cap : ops4);
