@@ -47,6 +47,7 @@ constexpr int V6_ROW0 = 2 + V6_NTOK;   // first dynamic-row slot
 // table slots: 0 = static A (sp = P), 1 = static B (sp = 0), 2..4 = tabulated
 // partial hits (sp = P - t), V6_ROW0+ = dynamic rows
 constexpr int V6_SLOTS = V6_RCAP + V6_ROW0;
+static_assert(V6_SLOTS <= 127, "class slots are stored as int8");
 constexpr int V6_KEY_ALWAYS = 999;     // op applied on every device (same-model, prefix)
 constexpr int V6_KEY_MODEL = 1000;     // op key >= this: displacement op of model key-1000
 constexpr int V6_KEY_SIGMA = 2000;     // OVR edge op: key-2000 = location, val = sigma
@@ -115,7 +116,7 @@ struct __align__(16) V6SmemT {
     double sw[DMX];
     double tr[DMX];
     int key[DMX];
-    int cslot[DMX];
+    int8_t cslot[DMX];  // class slot per device: -1 .. V6_SLOTS - 1
     int rowdev[V6_RCAP];
 };
 template <int DPL>
@@ -166,7 +167,7 @@ inline V6Layout v6_layout(int D, int Bmax, int max_level_ops, int n_models, bool
     L.opmask = take(ops4, maskw ? 8 : 4);
     L.mmask = take(maskw ? n_models : 0, 8);
     L.key = take(D, 4);
-    L.cslot = take(D, 4);
+    L.cslot = take(D, 1);
     L.rowdev = take(V6_RCAP, 4);
     L.item_bytes = o;
     return L;
@@ -461,7 +462,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     int* const s_opkey = reinterpret_cast<int*>(sb + lay.opmask);  // key walks: 4-byte keys
     unsigned* const s_mm = reinterpret_cast<unsigned*>(sb + lay.mmask);
     int* const s_key = SL ? ss->key : reinterpret_cast<int*>(sb + lay.key);
-    int* const s_cslot = SL ? ss->cslot : reinterpret_cast<int*>(sb + lay.cslot);
+    int8_t* const s_cslot = SL ? ss->cslot : reinterpret_cast<int8_t*>(sb + lay.cslot);
     int* const s_rowdev = SL ? ss->rowdev : reinterpret_cast<int*>(sb + lay.rowdev);
 
     const unsigned FULL = 0xffffffffu;
@@ -649,7 +650,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                  : (c > 0 && c < it.Pv && tokv.w > 2 && tt == tokv.z) ? 4
                                                                  : -2;
         }
-        if (ok[j] && sl >= 0) s_cslot[dv[j]] = sl;  // static class: slot known now
+        if (ok[j] && sl >= 0) s_cslot[dv[j]] = (int8_t)sl;  // static class: slot known now
         dyn[j] = ok[j] && sl == -2;
         unsigned same = __ballot_sync(FULL, dyn[j]);
         if (!per_device_rows) {
@@ -694,7 +695,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         if (!dyn[j]) continue;
         const int r = __popcll(dyn_m & low_mask(rep[j]));
         if (rep[j] == dv[j] && r < V6_RCAP) s_rowdev[r] = dv[j];
-        s_cslot[dv[j]] = r < V6_RCAP ? V6_ROW0 + r : -1;
+        s_cslot[dv[j]] = (int8_t)(r < V6_RCAP ? V6_ROW0 + r : -1);
     }
     if (stat_ok && t < 15) {
         // lane t holds the sums of static class si = t / 3 (A, B, T0, T1, T2),
