@@ -55,6 +55,8 @@ extern "C" {
 
 /* fate_bank.flags bits */
 #define FATE_BANK_UNIFORM_SPEED 1   /* every device has the same speed_factor */
+#define FATE_BANK_NO_QGROUPS 2      /* no query has a prefix group (q_group all -1);
+                                       lets fate_score run its lean kernel */
 
 /* fate_bank.st_flags bits */
 #define FATE_STAGE_CACHE_REUSE 1

@@ -229,7 +229,7 @@ __global__ void fate_prepare_demand_kernel(fate_bank b, fate_windows win, fate_d
 #include "fate_score_v5.cuh"
 #include "fate_score_v6.cuh"
 
-template <int DPL, bool OVR, bool SL, int MINB>
+template <int DPL, bool OVR, bool SL, int MINB, bool QG>
 int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                  const fate_derived* der, const fate_state* st, const fate_work* work,
                  const fate_out* out, cudaStream_t s) {
@@ -249,7 +249,7 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     const size_t smem = (size_t)lay.item_bytes * 4;
     if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v6 shared-memory footprint too large");
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fate_score_v6_kernel<DPL, OVR, SL, MINB>,
+        cudaFuncSetAttribute(fate_score_v6_kernel<DPL, OVR, SL, MINB, QG>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // persistent grid: every resident CTA slot once (capped by the item count)
     static thread_local size_t occ_smem = ~size_t(0);
@@ -257,11 +257,11 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     static thread_local const void* occ_fn = nullptr;
     int dev = 0;
     cudaGetDevice(&dev);
-    const void* fn = (const void*)fate_score_v6_kernel<DPL, OVR, SL, MINB>;
+    const void* fn = (const void*)fate_score_v6_kernel<DPL, OVR, SL, MINB, QG>;
     if (occ_smem != smem || occ_dev != dev || occ_fn != fn) {
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fate_score_v6_kernel<DPL, OVR, SL, MINB>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fate_score_v6_kernel<DPL, OVR, SL, MINB, QG>,
                                                       128, smem);
         o = std::max(1, sms * std::max(1, per));
         occ_smem = smem;
@@ -284,7 +284,7 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     static std::atomic<int> slot{0};
     const int qs = g_queue_slot_override >= 0 ? g_queue_slot_override
                                               : slot.fetch_add(1) % V6_QDIRECT;
-    fate_score_v6_kernel<DPL, OVR, SL, MINB><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
+    fate_score_v6_kernel<DPL, OVR, SL, MINB, QG><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
                                                                     *work, *out, lay, qs, fetch);
     return 0;
 }
@@ -328,11 +328,26 @@ int launch_v5(const fate_bank* bank, const fate_weights* w, const fate_windows* 
     }
 }
 
+// Lean instantiation (QG = false) when the caller declares that no query has a
+// prefix group (FATE_BANK_NO_QGROUPS) and the topology has no transfer
+// override: the per-device query-group paths compile out (configs 4/5:
+// 12 % less code, C4 -6.6 %, C5 -1.7 % on B200 -- the D = 64 kernel was
+// instruction-fetch bound).
+template <int DPL, bool SL, int MINB>
+int launch_v6_q(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+                const fate_derived* der, const fate_state* st, const fate_work* work,
+                const fate_out* out, cudaStream_t s) {
+    if (bank->has_overrides != 0)
+        return launch_v6_mb<DPL, true, SL, MINB, true>(bank, w, win, der, st, work, out, s);
+    if (bank->flags & FATE_BANK_NO_QGROUPS)
+        return launch_v6_mb<DPL, false, SL, MINB, false>(bank, w, win, der, st, work, out, s);
+    return launch_v6_mb<DPL, false, SL, MINB, true>(bank, w, win, der, st, work, out, s);
+}
+
 template <int DPL, bool SL>
 int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                  const fate_derived* der, const fate_state* st, const fate_work* work,
                  const fate_out* out, cudaStream_t s) {
-    const bool ovr = bank->has_overrides != 0;
     const char* e = getenv("FATE_MINB");
     // register budget (CTAs per SM), measured on B200: 10 for one device slot
     // per lane (48 registers: the extra warps hide more latency than the
@@ -340,15 +355,9 @@ int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_window
     // 7 x 72 registers once the chunked op buffer let 8 CTAs fit in shared
     // memory).  FATE_MINB = 7 | 8 | 10 selects another instantiation (A/B).
     switch (e ? atoi(e) : (DPL == 1 ? 10 : 8)) {
-        case 7:
-            return ovr ? launch_v6_mb<DPL, true, SL, 7>(bank, w, win, der, st, work, out, s)
-                       : launch_v6_mb<DPL, false, SL, 7>(bank, w, win, der, st, work, out, s);
-        case 10:
-            return ovr ? launch_v6_mb<DPL, true, SL, 10>(bank, w, win, der, st, work, out, s)
-                       : launch_v6_mb<DPL, false, SL, 10>(bank, w, win, der, st, work, out, s);
-        default:
-            return ovr ? launch_v6_mb<DPL, true, SL, 8>(bank, w, win, der, st, work, out, s)
-                       : launch_v6_mb<DPL, false, SL, 8>(bank, w, win, der, st, work, out, s);
+        case 7: return launch_v6_q<DPL, SL, 7>(bank, w, win, der, st, work, out, s);
+        case 10: return launch_v6_q<DPL, SL, 10>(bank, w, win, der, st, work, out, s);
+        default: return launch_v6_q<DPL, SL, 8>(bank, w, win, der, st, work, out, s);
     }
 }
 

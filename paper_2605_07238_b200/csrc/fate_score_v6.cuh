@@ -423,11 +423,13 @@ struct V6Item {
 
 // cache-aware query_compute of query q on device dv (costs.py:70-94) with the
 // device's effective stage part sp
+// (QG = false: the bank has no query prefix groups, FATE_BANK_NO_QGROUPS)
+template <bool QG>
 __device__ __forceinline__ double v6_qc(const fate_bank& b, const fate_state& st,
                                         const V6Item& it, const int* key, int dv, int q) {
     const long long sp = key[dv];
     long long qp = b.q_prompt[it.q0 + q];
-    const int qg = b.q_group[it.q0 + q];
+    const int qg = QG ? b.q_group[it.q0 + q] : -1;
     if (qg != -1) {
         const long long drow = it.dev_row0 + dv;
         const long long cc = cached_tokens(st.kappa + drow * it.cap4, st.kappa_n[drow], qg, it.m);
@@ -442,7 +444,7 @@ __device__ __forceinline__ double v6_qc(const fate_bank& b, const fate_state& st
 
 // One item (scenario, stage v) by one warp; sb = the warp's shared-memory slice
 // (static layout V6Static<DPL>::T when SL, else the runtime layout `lay`).
-template <int DPL, bool OVR, bool SL>
+template <int DPL, bool OVR, bool SL, bool QG>
 __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& w,
                                         const fate_windows& win, const fate_derived& der,
                                         const fate_state& st, const fate_work& work,
@@ -501,7 +503,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     const int bound = h2.z;
     const uint64_t elig = (uint64_t)h3.x;
     const bool cache_reuse = sflags & V6_CACHE_REUSE;
-    const bool per_device_rows = sflags & V6_QGROUPS;
+    const bool per_device_rows = QG && (sflags & V6_QGROUPS);
     it.pcoef = c0.x;
     it.pscale = c0.y;
     it.decode = c1.x;
@@ -715,7 +717,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     #pragma unroll 1
     for (int p = t; p < n_rows * nq; p += 32) {
         const int r = p / nq, q = p - r * nq;
-        s_rows[r * Bmax + q] = v6_qc(b, st, it, s_key, s_rowdev[r], q);
+        s_rows[r * Bmax + q] = v6_qc<QG>(b, st, it, s_key, s_rowdev[r], q);
     }
     __syncwarp();
     #pragma unroll 1
@@ -762,7 +764,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             } else {
                 PySum acc;
                 #pragma unroll 1
-                for (int q = 0; q < nq; ++q) acc.add(v6_qc(b, st, it, s_key, dv[j], q));
+                for (int q = 0; q < nq; ++q) acc.add(v6_qc<QG>(b, st, it, s_key, dv[j], q));
                 here[j] = acc.result();
             }
             if (!have || here[j] < bb) bb = here[j];
@@ -1077,7 +1079,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                         #pragma unroll 1
                         for (int q = lo; q < hi; ++q)
                             acc.add(slot >= V6_ROW0 ? s_rows[(slot - V6_ROW0) * Bmax + q]
-                                                    : v6_qc(b, st, it, s_key, dev, q));
+                                                    : v6_qc<QG>(b, st, it, s_key, dev, q));
                         ssum = acc.result();
                     }
                     const double tot = s_sw[dev] + s_tr[dev] + ssum;
@@ -1138,7 +1140,7 @@ constexpr int V6_QSLOTS = 256;
 constexpr int V6_QDIRECT = 128;
 __device__ unsigned int g_v6_queue[2 * V6_QSLOTS];  // per slot: next ticket, warps done
 
-template <int DPL, bool OVR, bool SL, int MINB>
+template <int DPL, bool OVR, bool SL, int MINB, bool QG>
 __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, fate_weights w,
                                                                   fate_windows win,
                                                                   fate_derived der, fate_state st,
@@ -1171,7 +1173,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
         const long long i1 = (long long)i + take < n ? (long long)i + take : n;
 #pragma unroll 1
         for (long long it = i; it < i1; ++it) {
-            v6_item<DPL, OVR, SL>(b, w, win, der, st, work, out, lay, it, sb);
+            v6_item<DPL, OVR, SL, QG>(b, w, win, der, st, work, out, lay, it, sb);
             __syncwarp();  // the slice is reused by the next item
         }
     }

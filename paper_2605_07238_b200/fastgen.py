@@ -161,7 +161,8 @@ def synth_batch(cfg, n_inst: int, seed0: int, scen0: int, depth: int, width: int
     scalars = dict(n_devices=D, n_models=len(catalog), n_roles=len(role_rows),
                    has_overrides=1 if len(topo.transfer_overrides) else 0, n_instances=n_inst,
                    n_stages=NS, n_edges=E, n_queries=n_inst * batch, max_queries=batch,
-                   flags=1 if bool(np.all(arrays["dev_speed"] == arrays["dev_speed"][0])) else 0,
+                   flags=(1 if bool(np.all(arrays["dev_speed"] == arrays["dev_speed"][0])) else 0)
+                   | (2 if not np.any(arrays["q_group"] != -1) else 0),
                    beta_default=float(topo.default_transfer_coeff))
     sids = sorted(f"s{n:02d}" for n in range(V))
     sindex = {s: i for i, s in enumerate(sids)}

@@ -41,6 +41,7 @@ ABL_BITS = {
     "no_shard": 16,
 }
 BANK_UNIFORM_SPEED = 1
+BANK_NO_QGROUPS = 2  # no query prefix group anywhere in the bank (lean kernel)
 STAGE_CACHE_REUSE = 1
 STAGE_KEEP_CACHE = 2
 
@@ -253,7 +254,8 @@ def pack_bank(instances, models, topo) -> PackedBank:
         n_devices=n_dev, n_models=len(catalog), n_roles=len(role_rows), has_overrides=has_over,
         n_instances=len(instances), n_stages=g0, n_edges=int(arrays["par_idx"].size),
         n_queries=len(q_prompt), max_queries=max_q, beta_default=float(topo.default_transfer_coeff),
-        flags=BANK_UNIFORM_SPEED if bool(np.all(speed == speed[0])) else 0,
+        flags=(BANK_UNIFORM_SPEED if bool(np.all(speed == speed[0])) else 0)
+        | (BANK_NO_QGROUPS if not np.any(arrays["q_group"] != -1) else 0),
     )
     return PackedBank(
         device_ids=device_ids, dev_index=dev_index, model_index=model_index,

@@ -224,3 +224,20 @@ def test_ptx_contraction_check_allows_only_tagged_exact_fmas():
     if os.path.exists(built):  # by-product of build(); the build itself also checks
         with open(built) as fh:
             assert build.ptx_contraction_free(fh.read())
+
+
+def test_bank_flags_declare_query_groups_exactly():
+    """FATE_BANK_NO_QGROUPS (the lean kernel) is set iff no query of the bank
+    has a prefix group -- by the object packer and by the native generator."""
+    from cases import token_case, wide_case
+    from paper_2605_07238_b200 import fastgen
+
+    c5 = c5_case(n_inst=2)
+    assert c5.bank.scalars["flags"] & pack.BANK_NO_QGROUPS
+    assert not np.any(c5.bank.arrays["q_group"] != -1)
+    assert token_case().bank.scalars["flags"] & pack.BANK_NO_QGROUPS
+    for case in (edge_case(), wide_case(33, 16, 3, False, 3)):
+        assert np.any(case.bank.arrays["q_group"] != -1)
+        assert not case.bank.scalars["flags"] & pack.BANK_NO_QGROUPS
+    fb = fastgen.synth_batch(scenarios.config_c5(), 2, 1000, 0, 20, 25, 0.12)
+    assert fb.bank.scalars["flags"] & pack.BANK_NO_QGROUPS
