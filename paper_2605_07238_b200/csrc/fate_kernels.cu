@@ -329,8 +329,9 @@ int launch_v5(const fate_bank* bank, const fate_weights* w, const fate_windows* 
 }
 
 // Lean instantiation (QG = false) when the caller declares that no query has a
-// prefix group (FATE_BANK_NO_QGROUPS) and the topology has no transfer
-// override: the per-device query-group paths compile out (configs 4/5:
+// prefix group (FATE_BANK_NO_QGROUPS) and every device has the same speed
+// (FATE_BANK_UNIFORM_SPEED), and the topology has no transfer override: the
+// per-device query-group and per-speed class paths compile out (configs 4/5:
 // 12 % less code, C4 -6.6 %, C5 -1.7 % on B200 -- the D = 64 kernel was
 // instruction-fetch bound).
 template <int DPL, bool SL, int MINB>
@@ -339,7 +340,7 @@ int launch_v6_q(const fate_bank* bank, const fate_weights* w, const fate_windows
                 const fate_out* out, cudaStream_t s) {
     if (bank->has_overrides != 0)
         return launch_v6_mb<DPL, true, SL, MINB, true>(bank, w, win, der, st, work, out, s);
-    if (bank->flags & FATE_BANK_NO_QGROUPS)
+    if ((bank->flags & FATE_BANK_NO_QGROUPS) && (bank->flags & FATE_BANK_UNIFORM_SPEED))
         return launch_v6_mb<DPL, false, SL, MINB, false>(bank, w, win, der, st, work, out, s);
     return launch_v6_mb<DPL, false, SL, MINB, true>(bank, w, win, der, st, work, out, s);
 }

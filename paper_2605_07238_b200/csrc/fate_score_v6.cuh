@@ -628,7 +628,8 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     int kb = 0, ki = 0, per = 0, n_rows = 0;
     bool kb_ok = false, ki_ok = false;
     unsigned long long dyn_m = 0ull;
-    const bool uniform = b.flags & FATE_BANK_UNIFORM_SPEED;
+    // the lean instantiation (QG = false) is only launched for uniform-speed banks
+    const bool uniform = !QG || (b.flags & FATE_BANK_UNIFORM_SPEED);
     const int n_idle = __popcll(idle_m);
     if (R > 1 && !no_shard) {
         kb = R < 1 + n_idle ? R : 1 + n_idle;

@@ -242,7 +242,7 @@ ALL_ABLATIONS = ("no_future_planning", "no_locality", "no_same_model", "no_prefi
 
 def wide_case(n_dev: int, n_queries: int, kappa: int, overrides: bool, horizon: int = 4,
               seed: int = 11, n_stages: int = 30, uniform_speed: bool = False,
-              n_scen: int = 3):
+              n_scen: int = 3, qgroups: bool = True):
     """Random layered DAG at the ABI's size limits: up to 64 devices (one or
     two device slots per lane, the 32/33 boundary), query batches past the
     static 16-query layout up to MAX_QUERIES, up to MAX_KAPPA prefix entries
@@ -292,8 +292,8 @@ def wide_case(n_dev: int, n_queries: int, kappa: int, overrides: bool, horizon: 
                             shared_prefix_group=groups[i % 4], keep_cache=bool(i % 2),
                             cache_reuse=bool(i % 3))
     dag = annotate_topology(WorkflowDag("wide", "wide", stages, frozenset(edges)))
-    qgroups = ["qa", "qb", "pg1", None]
-    queries = tuple(Query(f"q{i:03d}", 50 + rng.randrange(950), qgroups[i % 4])
+    qg_names = ["qa", "qb", "pg1", None] if qgroups else [None]
+    queries = tuple(Query(f"q{i:03d}", 50 + rng.randrange(950), qg_names[i % len(qg_names)])
                     for i in range(n_queries))
     inst = WorkflowInstance(dag=dag, queries=queries, batch_size=n_queries,
                             prefix_groups={"qa": 100, "qb": 700})

@@ -137,6 +137,19 @@ def test_wide_shapes(args):
     assert_parity(wide_case(*args))
 
 
+@pytest.mark.parametrize("uniform", [True, False])
+@pytest.mark.parametrize("n_dev", [32, 64])
+def test_no_query_groups_lean_and_general_kernels(uniform, n_dev):
+    """Banks without query prefix groups: uniform speed runs the lean
+    instantiation (FATE_BANK_NO_QGROUPS + FATE_BANK_UNIFORM_SPEED), mixed
+    speeds the general one; both bit-identical."""
+    case = wide_case(n_dev, 16, 4, False, 4, seed=9, uniform_speed=uniform, qgroups=False)
+    flags = case.bank.scalars["flags"]
+    assert flags & pack.BANK_NO_QGROUPS
+    assert bool(flags & pack.BANK_UNIFORM_SPEED) == uniform
+    assert_parity(case)
+
+
 def test_wide_shapes_uniform_speed_ablations():
     for flag in ALL_ABLATIONS:
         case = wide_case(64, 16, 3, False, 4, seed=5, uniform_speed=True)
