@@ -241,3 +241,35 @@ def test_bank_flags_declare_query_groups_exactly():
         assert not case.bank.scalars["flags"] & pack.BANK_NO_QGROUPS
     fb = fastgen.synth_batch(scenarios.config_c5(), 2, 1000, 0, 20, 25, 0.12)
     assert fb.bank.scalars["flags"] & pack.BANK_NO_QGROUPS
+
+
+def test_c_abi_from_plain_c(tmp_path):
+    """examples/solve_frontier.c links libfate.so from C (no Python) and its
+    native solve equals the Python restatement of the reference's
+    solve_frontier on the same problem (selection, objective, node count)."""
+    import shutil
+    import subprocess
+
+    from paper_2605_07238_b200.wf.frontier import Candidate as Cd
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    lib_dir = os.path.join(ROOT, "paper_2605_07238_b200")
+    exe = str(tmp_path / "solve_frontier")
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "solve_frontier.c"), "-L", lib_dir, "-lfate",
+                    f"-Wl,-rpath,{lib_dir}", "-o", exe], check=True)
+    line = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.strip()
+    fields = dict(kv.split("=", 1) for kv in line.split())
+    cands = [Cd("s0", 0, "d0", 5.0), Cd("s0", 0, "d1", 3.0), Cd("s0", 1, "d0", 0.5),
+             Cd("s0", 1, "d1", 0.25), Cd("s1", 0, "d0", 4.0), Cd("s1", 0, "d1", 6.0),
+             Cd("s2", 0, "d2", -1.0)]
+    want = solve_frontier(FrontierProblem(candidates=tuple(cands),
+                                          shard_bounds={"s0": 2, "s1": 1, "s2": 1},
+                                          device_ids=("d0", "d1", "d2")), budget_s=0.25)
+    got = tuple(tuple(int(x) for x in t.split(":")) for t in fields["sel"].split(","))
+    assert got == tuple((int(s[1:]), k, int(d[1:])) for s, k, d in want.selected)
+    assert float(fields["objective"]) == want.objective
+    assert int(fields["optimal"]) == int(want.optimal)
+    assert int(fields["nodes"]) == want.nodes_explored
+    assert int(fields["abi"]) == runtime.load_library().fate_abi_version()
