@@ -13,7 +13,8 @@ cfg, bank, states, work, _ = bench.build_c5(0, 1, "frontier")
 dbank = runtime.DeviceBank(bank, cfg.weights, device=dev)
 for chunks in [int(x) for x in (sys.argv[1:] or ["1", "8"])]:
     print("chunks", chunks, file=sys.stderr, flush=True)
-    pipe = runtime.HostPipeline(dbank, states, work, n_chunks=chunks, n_streams=1)
+    pipe = runtime.HostPipeline(dbank, states, work, n_chunks=chunks,
+                                n_streams=int(os.environ.get("TRACE_STREAMS", "3")))
     for _ in range(2):
         pipe.run()
     torch.cuda.synchronize()
