@@ -532,8 +532,9 @@ def run_fate(args):
     torch.cuda.synchronize(device)
 
     clocks = ClockSampler(local)
+    # one rank has nothing to gather (and no process group at N = 1)
     ms, launches = time_device(torch, dbank, dstates, dwork, out, args.steps, args.warmup, flush,
-                               world, device, gather=args.gather, clocks=clocks)
+                               world, device, gather=args.gather and world > 1, clocks=clocks)
     ms_max = reduce_max(ms, world, device)
     psi_total = reduce_sum(float(work.n_psi), world, device)
     value = psi_total / (ms_max / 1e3)
@@ -588,7 +589,8 @@ def run_fate(args):
                 "parallelism": f"dp{world}: "
                                + ("instances" if args.workload == "c5" else "scenario seeds")
                                + " sharded by rank, no data-path collective"
-                               + (" + NCCL all-gather of Psi" if args.gather else ""),
+                               + (" + NCCL all-gather of Psi" if args.gather and world > 1
+                                  else ""),
             },
             "roofline": roofline,
             "cpu_baseline": cpu,
