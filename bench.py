@@ -2,33 +2,39 @@
 """FATE candidate-scoring benchmark (B200).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fate|reference]
-                    [--workload c5|c4] [--mode frontier|sweep] [--gather]
+                    [--workload c5|c4] [--mode frontier|sweep]
 
 One *step* = one pass of the hot path (horizon-aware candidate scoring +
 state-conditional cost estimation, i.e. ``build_problem``'s Psi matrix plus
 the S and completion matrices) over one batch of synthetic input.
 
 Default workload (BASELINE.json configs[4], "c5"): 4096 independent
-synthetic workflow instances (500 stages, 32 devices, H=3) per GPU, one
-canonical scenario state each, every ready-frontier (stage x slot x device)
-candidate scored -- 5.72 M Psi per GPU per step.  Multi-GPU: one process per
-GPU (torchrun), each rank scores its own 4096 instances (instance seeds offset
-by rank): independent units, no data-path collective, weak scaling.
-``--gather`` adds an NCCL all-gather of the per-rank Psi slabs to every rank.
+synthetic workflow instances (500 stages, 32 devices, H=3), one canonical
+scenario state each, every ready-frontier (stage x slot x device) candidate
+scored -- 5.72 M Psi per step.  Multi-GPU: one process per GPU
+(torchrun); rank r owns the contiguous instances [r*4096/N, (r+1)*4096/N)
+(strong scaling, the headline); per step each rank scores its shard, the
+per-rank Psi slabs are all-gathered over NCCL, each rank solves its
+instances' frontiers on its host cores (native budget-0 solve, timed
+separately) and the per-instance assignment triples are all-gathered over
+NCCL.  ``weak`` (N > 1) repeats the kernel timing with 4096 instances per
+rank.
 
-Also measured in the same run (N=1): config 4 ("c4_sweep": the 10k-stage,
+Also measured in the same run: config 4 ("c4_sweep": the 10k-stage,
 64-device, 8-model, H=4 DAG, all stages x 8 scenario states, 9.0 M Psi per
-step), the north-star roofline kernel.
+step, scenarios split 8/N per rank), the north-star roofline kernel.
 
 Timing: CUDA events on the launching stream around each scoring launch,
 inputs HBM-resident, L2 flushed (256 MiB write) between steps outside the
 events; max over ranks.  ``e2e`` = the same work through the host-buffer call
 ``fate_pipeline`` (pinned H2D of the step's scenario records, loc rows and
 work items, unpack + scoring kernels, D2H of Psi), captured once into a CUDA
-graph and replayed every step.
+graph and replayed every step, plus (N > 1) the NCCL all-gathers of the Psi
+slabs and of the assignment triples.
 ``cpu_baseline`` / ``--impl reference`` = the C oracle port of the
 reference scorer on the host cores (test-infrastructure checker, never the
-product path).
+product path); the reference arm builds its inputs with the reference's own
+generators (``wfsched`` from baseline/_ref) and never loads libfate.so.
 """
 
 from __future__ import annotations
@@ -46,7 +52,7 @@ if ROOT not in sys.path:
 
 METRIC = "candidate assignments scored/sec (stage×device×horizon)"
 UNIT = "candidates/s"
-PER_GPU_INSTANCES = 4096
+TOTAL_INSTANCES = 4096
 C5_SHAPE = dict(depth=20, width=25, density=0.12, batch=16)
 C4_SCENARIOS = 8
 HBM_FALLBACK_GBS = 6650.0
@@ -64,11 +70,25 @@ def dist_env():
     return rank, world, local
 
 
-def shard_plan(rank: int, world: int, per_gpu: int = PER_GPU_INSTANCES) -> dict:
-    """Weak scaling: rank r owns instances [r*per_gpu, (r+1)*per_gpu); config-5
-    instance i uses synth seed 1000+i and scenario seed i."""
-    first = rank * per_gpu
-    return {"first": first, "count": per_gpu, "seed0": 1000 + first, "scen0": first}
+def shard_plan(rank: int, world: int, total: int = TOTAL_INSTANCES,
+               scaling: str = "strong") -> dict:
+    """Config-5 instance shard of a rank: strong scaling =
+    contiguous ranges of ``total``/world instances; weak = ``total`` instances
+    per rank, offset by rank.  Instance i uses synth seed 1000+i and scenario
+    seed i."""
+    if scaling == "strong":
+        lo, hi = rank * total // world, (rank + 1) * total // world
+        first, count = lo, hi - lo
+    else:
+        first, count = rank * total, total
+    return {"first": first, "count": count, "seed0": 1000 + first, "scen0": first,
+            "scaling": scaling}
+
+
+def c4_plan(rank: int, world: int, n_scen: int = C4_SCENARIOS) -> tuple:
+    """Config-4 scenario seeds of a rank: contiguous ranges of n_scen/world."""
+    lo, hi = rank * n_scen // world, (rank + 1) * n_scen // world
+    return lo, hi - lo
 
 
 def reduce_max(value: float, world: int, device=None) -> float:
@@ -93,20 +113,41 @@ def reduce_sum(value: float, world: int, device=None) -> float:
     return float(t.item())
 
 
-def gather_slabs(psi, world: int):
-    """NCCL all-gather of per-rank Psi slabs (padded to the largest)."""
-    import torch
-    import torch.distributed as dist
+class SlabGather:
+    """NCCL all-gather of equally sized per-rank slabs (padded to the largest
+    rank's size, agreed once): every rank ends up with all ranks' slabs."""
 
-    n = torch.tensor([psi.numel()], dtype=torch.int64, device=psi.device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n)
-    m = int(max(int(s.item()) for s in sizes))
-    pad = torch.full((m,), float("nan"), dtype=psi.dtype, device=psi.device)
-    pad[: psi.numel()] = psi
-    out = torch.empty(world * m, dtype=psi.dtype, device=psi.device)
-    dist.all_gather_into_tensor(out, pad)
-    return out, [int(s.item()) for s in sizes]
+    def __init__(self, torch, n_local: int, dtype, device, world: int, fill=0):
+        import torch.distributed as dist
+
+        n = torch.tensor([n_local], dtype=torch.int64, device=device)
+        sizes = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(sizes, n)
+        self.sizes = [int(x.item()) for x in sizes]
+        self.m = max(max(self.sizes), 1)
+        self.slab = torch.full((self.m,), fill, dtype=dtype, device=device)
+        self.out = torch.empty(world * self.m, dtype=dtype, device=device)
+        self.n_local = n_local
+        self.bytes = world * self.m * self.slab.element_size()
+
+    def __call__(self, local):
+        import torch.distributed as dist
+
+        self.slab[: self.n_local].copy_(local[: self.n_local])
+        dist.all_gather_into_tensor(self.out, self.slab)
+        return self.out
+
+    def part(self, r: int):
+        return self.out[r * self.m: r * self.m + self.sizes[r]]
+
+
+def gather_slabs(psi, world: int):
+    """One-shot all-gather of per-rank slabs (padded to the largest)."""
+    import torch
+
+    g = SlabGather(torch, psi.numel(), psi.dtype, psi.device, world, fill=float("nan"))
+    out = g(psi)
+    return out, g.sizes
 
 
 # ---------------------------------------------------------------------------
@@ -175,17 +216,16 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def build_c5(rank: int, world: int, mode: str):
+def build_c5(plan: dict, mode: str):
     from paper_2605_07238_b200 import fastgen, pack, scenarios
 
-    plan = shard_plan(rank, world)
     cfg = scenarios.config_c5()
     fb = fastgen.synth_batch(cfg, plan["count"], plan["seed0"], plan["scen0"],
                              C5_SHAPE["depth"], C5_SHAPE["width"], C5_SHAPE["density"],
                              C5_SHAPE["batch"])
     sc, g = fb.frontier_items() if mode == "frontier" else fb.sweep_items()
     work = pack.make_work(fb.bank, zip(sc.tolist(), g.tolist()), cfg.weights.ablation.no_shard)
-    return cfg, fb.bank, fb.states, work, plan
+    return cfg, fb.bank, fb.states, work
 
 
 def build_c4(mode: str = "sweep", n_scen: int = C4_SCENARIOS, first_scen: int = 0):
@@ -224,6 +264,37 @@ def build_c4(mode: str = "sweep", n_scen: int = C4_SCENARIOS, first_scen: int = 
             items += [(s, int(x)) for x in g]
     work = pack.make_work(bank, items, cfg.weights.ablation.no_shard)
     return cfg, bank, states, work
+
+
+def workload_config(args, world: int) -> dict:
+    """The ``config`` object of the bench line -- static, identical for both
+    arms (measured quantities live outside it)."""
+    if args.workload == "c5":
+        return {"workload": f"c5_{args.mode}", "instances": TOTAL_INSTANCES,
+                "stages_per_instance": 500, "devices": 32, "batch": C5_SHAPE["batch"],
+                "horizon": 3, "scenario_states": "canonical (SURVEY §8(d)), one per instance",
+                "l2": "flushed between steps (256 MiB write, outside the events)",
+                "parallelism": f"dp{world}: contiguous instance ranges of {TOTAL_INSTANCES}"
+                               f"/{world} per rank (strong scaling); NCCL all-gather of Psi "
+                               "slabs and assignment triples"}
+    return {"workload": f"c4_{args.mode}", "instances": 1, "stages_per_instance": 10000,
+            "devices": 64, "batch": 16, "horizon": 4, "scenario_states": C4_SCENARIOS,
+            "l2": "flushed between steps (256 MiB write, outside the events)",
+            "parallelism": f"dp{world}: scenario seeds {C4_SCENARIOS}/{world} per rank "
+                           "(strong scaling)"}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 # ---------------------------------------------------------------------------
@@ -284,7 +355,7 @@ def issue_ceiling(key: str, ms: float, sm_mhz) -> dict | None:
 
 
 def time_device(torch, dbank, dstates, dwork, out, steps, warmup, flush, world, device,
-                gather=False, clocks=None):
+                clocks=None):
     """Per-step kernel time (CUDA events on the launching stream), L2 flushed
     between steps outside the events.  Returns (ms_per_step, launches)."""
     import torch.distributed as dist
@@ -295,8 +366,6 @@ def time_device(torch, dbank, dstates, dwork, out, steps, warmup, flush, world, 
     for _ in range(warmup):
         flush.fill_(1.0)
         dbank.score_into(dstates, dwork, out)
-        if gather:
-            gather_slabs(out.psi, world)
     torch.cuda.synchronize(device)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(steps)]
@@ -310,8 +379,6 @@ def time_device(torch, dbank, dstates, dwork, out, steps, warmup, flush, world, 
             flush.fill_(float(i))
             ev[i][0].record(stream)
             dbank.score_into(dstates, dwork, out)
-            if gather:
-                gather_slabs(out.psi, world)
             ev[i][1].record(stream)
         torch.cuda.synchronize(device)
     launches = runtime.launch_count() - launches0
@@ -329,16 +396,16 @@ class _Null:
         return False
 
 
-def time_e2e(torch, pipe, steps, warmup, world, device, blocks: int = 5):
-    """ms per step of the host-buffer pipeline: ``steps`` back-to-back replays
-    timed with CUDA events in ``blocks`` equal blocks; the median block is
-    reported (PCIe transfers see occasional host-side hiccups) together with
-    every block's value."""
+def time_e2e(torch, step, steps, warmup, world, device, blocks: int = 5):
+    """ms per step of the host-buffer path ``step()``: ``steps`` back-to-back
+    steps timed with CUDA events in ``blocks`` equal blocks; the median block
+    is reported (PCIe transfers see occasional host-side hiccups) together
+    with every block's value."""
     import torch.distributed as dist
 
     stream = torch.cuda.current_stream(device)
     for _ in range(warmup):
-        pipe.run()
+        step()
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
@@ -348,58 +415,90 @@ def time_e2e(torch, pipe, steps, warmup, world, device, blocks: int = 5):
     ev[0].record(stream)
     for b in range(blocks):
         for _ in range(per):
-            pipe.run()
+            step()
         ev[b + 1].record(stream)
     torch.cuda.synchronize(device)
     ms = sorted(ev[b].elapsed_time(ev[b + 1]) / per for b in range(blocks))
     return ms[len(ms) // 2], ms
 
 
-def measure_host_solve(bank, work, psi_host, n_inst: int = 16) -> dict:
-    """Host frontier solve of the first ``n_inst`` config-5 instances on the
-    GPU cost matrix (outside every timed region): the reference's solve
-    restated in Python vs the native ``fate_solve_frontier``, both at budget 0
-    (option enumeration + deterministic greedy -- a full search of a 25-stage,
-    32-device frontier does not finish in either), selections compared."""
+def problem_ptr(work, key):
+    """Work items -> problems (one (instance, scenario) frontier each): items
+    are scenario-major in stage order, so a problem is a contiguous run."""
     import numpy as np
 
-    from paper_2605_07238_b200 import solver as native
-    from paper_2605_07238_b200.wf import frontier as MF
+    k = np.asarray(key)
+    starts = np.flatnonzero(np.r_[True, k[1:] != k[:-1]]) if len(k) else np.zeros(0, int)
+    return np.r_[starts, len(k)].astype(np.int32)
+
+
+def host_solve_all(bank, work, psi_host, threads: int = 0, repeats: int = 3) -> tuple:
+    """Native budget-0 host solve (fate_solve_batch) of every frontier of the
+    rank's batch on its host threads -- timed separately from the GPU path
+    (north star).  Returns (summary, BatchSolution)."""
+    import numpy as np
+
+    from paper_2605_07238_b200 import solver
+
+    ptr = problem_ptr(work, work.scen)
+    elig = bank.arrays["st_elig"][np.asarray(work.stage)]
+    walls, sol = [], None
+    for _ in range(repeats):
+        sol = solver.solve_batch(ptr, work.bounds, elig, work.psi_off, psi_host,
+                                 bank.scalars["n_devices"], budget_s=0.0, n_threads=threads)
+        walls.append(sol.wall_s)
+    walls.sort()
+    return ({"problems": len(ptr) - 1, "budget_s": 0.0, "threads": sol.threads,
+             "ms_per_step": 1e3 * walls[len(walls) // 2],
+             "ms_per_problem": 1e3 * walls[len(walls) // 2] / max(1, len(ptr) - 1),
+             "optimal": int(sol.optimal.sum()), "solver": "fate_solve_batch (native, "
+             "restates planner.py:101-234), host threads"}, sol)
+
+
+def reference_solve_check(bank, work, psi_host, sol, n_check: int = 8) -> dict | None:
+    """The reference's own ``solve_frontier`` on the first instances' GPU cost
+    matrices selects exactly what the native batch solve selected (needs the
+    reference package; outside every timed region)."""
+    import numpy as np
+
+    try:
+        import wfsched.planner as RP
+    except ImportError:
+        return None
+    from paper_2605_07238_b200 import pack
 
     D = bank.scalars["n_devices"]
-    elig = bank.arrays["st_elig"]
-    sc = np.asarray(work.scen)
-    devs = tuple(f"d{j:02d}" for j in range(D))
-    t_py = t_nat = 0.0
+    ptr = problem_ptr(work, work.scen)
     same = True
-    n_cand = 0
-    for inst in range(n_inst):
+    t = 0.0
+    n = min(n_check, len(ptr) - 1)
+    for p in range(n):
+        items = range(ptr[p], ptr[p + 1])
+        inst = int(bank.arrays["st_inst"][int(work.stage[ptr[p]])])
+        sids = bank.stage_ids[inst]
+        off0 = int(bank.inst_stage_off[inst])
         cands, bounds = [], {}
-        for w in np.nonzero(sc == inst)[0]:
+        for w in items:
             g = int(work.stage[w])
-            sid = f"s{g:08d}"
+            sid = sids[g - off0]
             bounds[sid] = int(work.bounds[w])
-            m = int(elig[g])
-            base = int(work.psi_off[w])
+            m = int(bank.arrays["st_elig"][g])
             for k in range(bounds[sid]):
                 for d in range(D):
                     if m >> d & 1:
-                        cands.append(MF.Candidate(sid, k, devs[d], float(psi_host[base + k * D + d])))
-        prob = MF.FrontierProblem(tuple(cands), bounds, devs)
-        n_cand += len(cands)
+                        cands.append(RP.Candidate(sid, k, bank.device_ids[d],
+                                                  float(psi_host[int(work.psi_off[w]) + k * D + d])))
+        prob = RP.FrontierProblem(tuple(cands), bounds, tuple(bank.device_ids))
         t0 = time.perf_counter()
-        a = MF.solve_frontier(prob, budget_s=0.0)
-        t1 = time.perf_counter()
-        b = native.solve_frontier(prob, budget_s=0.0)
-        t2 = time.perf_counter()
-        t_py += t1 - t0
-        t_nat += t2 - t1
-        same &= (a.selected, a.objective.hex(), a.optimal) == (b.selected, b.objective.hex(),
-                                                               b.optimal)
-    return {"instances": n_inst, "candidates_per_instance": n_cand / n_inst, "budget_s": 0.0,
-            "python_ms_per_instance": 1e3 * t_py / n_inst,
-            "native_ms_per_instance": 1e3 * t_nat / n_inst, "identical": bool(same),
-            "note": "host solve timed separately (north star); reference semantics restated"}
+        ref = RP.solve_frontier(prob, budget_s=0.0)
+        t += time.perf_counter() - t0
+        got = tuple(sorted((sids[int(work.stage[a]) - off0], int(b), bank.device_ids[c])
+                           for a, b, c in sol.selected(p)))
+        same &= got == ref.selected and float(sol.objective[p]).hex() == ref.objective.hex()
+    _ = pack
+    return {"instances": n, "identical": bool(same),
+            "reference_ms_per_problem": 1e3 * t / max(n, 1),
+            "reference": "wfsched.planner.solve_frontier (Python), budget 0"}
 
 
 def cpu_sample_rate(bank, weights, states, work, target_s: float = 12.0, threads: int = 0):
@@ -435,6 +534,7 @@ def cpu_sample_rate(bank, weights, states, work, target_s: float = 12.0, threads
     oracle.score(bank, wrec, states, w, n_threads=threads, with_extras=False)
     dt = time.perf_counter() - t0
     return {"value": w.n_psi / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "cpu": cpu_model(),
             "sample": f"first {n2} of {work.n_items} work items ({w.n_psi} Psi) in {dt:.1f} s; "
                       f"C oracle (faithful port of CostModel.plan_score), OpenMP"}
 
@@ -444,61 +544,109 @@ def cpu_sample_rate(bank, weights, states, work, target_s: float = 12.0, threads
 # ---------------------------------------------------------------------------
 
 
+def _reference_pool(n_pool: int):
+    """Config-5 instances and their canonical scenario states built with the
+    reference's OWN generators and state type (wfsched, installed unmodified
+    in baseline/_ref), packed by the pure-Python packer: no libfate.so."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "wfsched")) and ref not in sys.path:
+        sys.path.append(ref)
+    import wfsched.benchgen as RB
+
+    from paper_2605_07238_b200 import pack, scenarios
+
+    cfg = scenarios.config_c5()
+    insts, states, items = [], [], []
+    for i in range(n_pool):
+        dag = RB.synth_generate(RB.SuiteSpec(kind="synthetic", depth=C5_SHAPE["depth"],
+                                             width=C5_SHAPE["width"],
+                                             density=C5_SHAPE["density"], seed=1000 + i,
+                                             batch_size=C5_SHAPE["batch"]), cfg)
+        insts.append(RB.make_instance(dag, C5_SHAPE["batch"], 1000 + i))
+    bank = pack.pack_bank(insts, cfg.models, cfg.topology)
+    for i, inst in enumerate(insts):
+        st = scenarios.build_scenario(inst, cfg, i)
+        states.append((i, st))
+        items += [(i, bank.global_index(i, sid)) for sid in scenarios.scenario_frontier(inst, st)]
+    return cfg, bank, pack.pack_states(bank, states), items
+
+
 def run_reference(args):
-    """Reference arm: the reference's CPU scorer (C oracle port) on the host
-    cores, same workload/metric; rank 0 only."""
+    """Reference arm: the reference's CPU scorer (the C oracle port of
+    ``CostModel.plan_score``) on the host cores, same metric and config as the
+    fate arm; rank 0 only.  Inputs come from the reference's own generators
+    (``_reference_pool``): this arm never loads libfate.so."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     import numpy as np
 
     import oracle
-    from paper_2605_07238_b200 import fastgen, pack, scenarios
+    from paper_2605_07238_b200 import pack
 
-    plan = shard_plan(0, 1)
-    cfg = scenarios.config_c5()
-    fb = fastgen.synth_batch(cfg, plan["count"], plan["seed0"], plan["scen0"],
-                             C5_SHAPE["depth"], C5_SHAPE["width"], C5_SHAPE["density"],
-                             C5_SHAPE["batch"])
-    sc, g = fb.frontier_items() if args.mode == "frontier" else fb.sweep_items()
+    if args.workload != "c5":
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "reference arm measured on the headline workload c5 only"}))
+        return 0
+    t0 = time.perf_counter()
+    cfg, bank, states, items = _reference_pool(args.ref_pool)
+    gen_s = time.perf_counter() - t0
     wrec = pack.weights_record(cfg.weights)
     threads = oracle.max_threads()
     per_step = args.ref_instances
-    inst_of = sc
+    inst_of = np.asarray([s for s, _ in items])
 
     def step_work(i):
-        lo = (i * per_step) % plan["count"]
-        sel = (inst_of >= lo) & (inst_of < lo + per_step)
-        return pack.make_work(fb.bank, zip(sc[sel].tolist(), g[sel].tolist()), False)
+        lo = (i * per_step) % args.ref_pool
+        sel = [it for it, s in zip(items, inst_of) if lo <= s < lo + per_step]
+        return pack.make_work(bank, sel, False)
 
     for i in range(args.warmup):
-        oracle.score(fb.bank, wrec, fb.states, step_work(i), n_threads=threads, with_extras=False)
+        oracle.score(bank, wrec, states, step_work(i), n_threads=threads, with_extras=False)
     works = [step_work(args.warmup + i) for i in range(args.steps)]
     n_psi = 0
     t0 = time.perf_counter()
     for w in works:
-        oracle.score(fb.bank, wrec, fb.states, w, n_threads=threads, with_extras=False)
+        oracle.score(bank, wrec, states, w, n_threads=threads, with_extras=False)
         n_psi += w.n_psi
     dt = time.perf_counter() - t0
     value = n_psi / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (config-5 generator, canonical scenario states)",
-        "config": {"workload": f"c5_{args.mode}", "instances_per_step": per_step,
-                   "stages_per_instance": 500, "devices": 32, "batch": 16, "horizon": 3},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generators wfsched.benchgen, canonical scenario states)",
+        "config": workload_config(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{per_step} instances' {args.mode} items per step, "
-                                   f"{n_psi} Psi over {args.steps} steps; C oracle port of "
-                                   f"CostModel.plan_score (OpenMP)"},
+                         "cpu": cpu_model(),
+                         "sample": f"each step: the full frontiers of {per_step} of the "
+                                   f"{TOTAL_INSTANCES} config-5 instances (a rotating window "
+                                   f"over instances 0..{args.ref_pool - 1}, built with the "
+                                   f"reference's generators in {gen_s:.1f} s); {n_psi} Psi "
+                                   f"over {args.steps} steps; C oracle port of "
+                                   f"CostModel.plan_score, OpenMP"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def _roofline(pack, runtime, bank, work, states, dbank, ms, key, sm_mhz):
+    nbytes = pack.compulsory_bytes(bank, work, states, dbank.levels,
+                                   runtime.build_windows(bank, dbank.levels))
+    ach = nbytes / (ms / 1e3) / 1e9
+    peak, peak_src = hbm_peak()
+    roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": traffic_for(key), "peak_source": peak_src, "bytes_per_launch": nbytes,
+            "bytes_per_candidate": nbytes / max(1, work.n_psi), "kernel": "fate_score_v6_kernel"}
+    ceil = issue_ceiling(key, ms, sm_mhz)
+    if ceil is not None:
+        roof["issue_ceiling"] = ceil
+    return roof
+
+
 def run_fate(args):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -509,12 +657,17 @@ def run_fate(args):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     device = torch.device(f"cuda:{local}")
     torch.cuda.set_device(device)
+    nvtx = torch.cuda.nvtx
 
+    nvtx.range_push("pack")
     if args.workload == "c5":
-        cfg, bank, states, work, plan = build_c5(rank, world, args.mode)
+        plan = shard_plan(rank, world, scaling="strong")
+        cfg, bank, states, work = build_c5(plan, args.mode)
     else:
-        cfg, bank, states, work = build_c4(args.mode, first_scen=rank * C4_SCENARIOS)
-        plan = None
+        first, n_scen = c4_plan(rank, world)
+        cfg, bank, states, work = build_c4(args.mode, n_scen=n_scen, first_scen=first)
+        plan = {"first": first, "count": n_scen}
+    nvtx.range_pop()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -532,76 +685,121 @@ def run_fate(args):
     torch.cuda.synchronize(device)
 
     clocks = ClockSampler(local)
-    # one rank has nothing to gather (and no process group at N = 1)
     ms, launches = time_device(torch, dbank, dstates, dwork, out, args.steps, args.warmup, flush,
-                               world, device, gather=args.gather and world > 1, clocks=clocks)
+                               world, device, clocks=clocks)
     ms_max = reduce_max(ms, world, device)
     psi_total = reduce_sum(float(work.n_psi), world, device)
     value = psi_total / (ms_max / 1e3)
-
-    levels = dbank.levels
-    nbytes = pack.compulsory_bytes(bank, work, states, levels, runtime.build_windows(bank, levels))
-    ach = nbytes / (ms / 1e3) / 1e9
-    peak, peak_src = hbm_peak()
-    key = f"{args.workload}_{args.mode}"
-    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": traffic_for(key), "peak_source": peak_src,
-                "bytes_per_launch": nbytes, "bytes_per_candidate": nbytes / work.n_psi,
-                "kernel": "fate_score_kernel"}
     csum = clocks.summary()
-    ceil = issue_ceiling(key, ms, csum.get("sm_mhz") or csum.get("sm_max_mhz"))
-    if ceil is not None:
-        roofline["issue_ceiling"] = ceil
+    key = f"{args.workload}_{args.mode}"
+    roofline = _roofline(pack, runtime, bank, work, states, dbank, ms, key,
+                         csum.get("sm_mhz") or csum.get("sm_max_mhz"))
 
+    # ---- end to end: host buffers -> GPU -> host, + NCCL gathers (N > 1) -------------
     pipe = runtime.HostPipeline(dbank, states, work, extras=False, n_chunks=4, graph=True)
-    e2e_ms, e2e_blocks = time_e2e(torch, pipe, max(10, args.steps), min(args.warmup, 3), world,
-                                  device)
+    psi_host = pipe.host_psi.numpy()
+    torch.cuda.synchronize(device)
+    # host solve of this rank's frontiers on its cores (timed separately)
+    solve, sol = (None, None)
+    if args.mode == "frontier":
+        nvtx.range_push("host_solve")
+        solve, sol = host_solve_all(bank, work, psi_host)
+        nvtx.range_pop()
+    psi_gather = assign_gather = None
+    if world > 1:
+        psi_gather = SlabGather(torch, work.n_psi, torch.float64, device, world,
+                                fill=float("nan"))
+        D = bank.scalars["n_devices"]
+        n_prob = len(sol.n_sel) if sol is not None else 0
+        trip = np.zeros((max(n_prob, 1), D * 3 + 1), dtype=np.int32)
+        if sol is not None:
+            trip[:n_prob, 0] = sol.n_sel
+            trip[:n_prob, 1:] = sol.sel.reshape(n_prob, D * 3)
+        assign_host = torch.from_numpy(trip.ravel()).pin_memory()
+        assign_dev = torch.empty_like(assign_host, device=device)
+        assign_gather = SlabGather(torch, assign_host.numel(), torch.int32, device, world)
+        assign_back = torch.empty(assign_gather.out.numel(), dtype=torch.int32, pin_memory=True)
+        dpsi = pipe.device_psi()
+
+    def e2e_step():
+        nvtx.range_push("e2e_step")
+        pipe.run()
+        if world > 1:
+            psi_gather(dpsi)
+            assign_dev.copy_(assign_host, non_blocking=True)
+            assign_gather(assign_dev)
+            assign_back.copy_(assign_gather.out, non_blocking=True)
+        nvtx.range_pop()
+
+    e2e_ms, e2e_blocks = time_e2e(torch, e2e_step, max(10, args.steps), min(args.warmup, 3),
+                                  world, device)
     e2e_max = reduce_max(e2e_ms, world, device)
+    h2d = pipe.h2d_bytes + (assign_host.numel() * 4 if world > 1 else 0)
+    d2h = pipe.d2h_bytes + (assign_back.numel() * 4 if world > 1 else 0)
     e2e = {"value": psi_total / (e2e_max / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": pipe.h2d_bytes, "d2h_bytes_per_step": pipe.d2h_bytes,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": e2e_max, "block_ms": e2e_blocks,
            "path": "fate_pipeline_capture/replay: 4 scenario-aligned chunks, H2D / scoring / "
-                   "D2H overlapped on 3 streams, one CUDA-graph launch per step"}
+                   "D2H overlapped on 3 streams, one CUDA-graph launch per step"
+                   + ("; then NCCL all_gather_into_tensor of the padded per-rank Psi slabs "
+                      f"({psi_gather.bytes} B) and of the per-instance assignment triples "
+                      f"({assign_gather.bytes} B, H2D before / D2H after)" if world > 1 else "")}
+    if world > 1:
+        # the gathered Psi slab of every rank equals that rank's own scores
+        torch.cuda.synchronize(device)
+        mine = psi_gather.part(rank).cpu().numpy()
+        e2e["gather_check"] = bool(np.array_equal(mine.view(np.uint64),
+                                                  psi_host[: work.n_psi].view(np.uint64)))
+    if solve is not None:
+        solve["ms_per_step_max_over_ranks"] = reduce_max(solve["ms_per_step"], world, device)
+        if rank == 0:
+            chk = reference_solve_check(bank, work, psi_host, sol)
+            if chk is not None:
+                solve["reference_check"] = chk
 
-    host_solve = None
-    if rank == 0 and world == 1 and args.workload == "c5" and args.mode == "frontier":
-        host_solve = measure_host_solve(bank, work, out.psi.cpu().numpy())
+    weak = None
+    if world > 1 and args.workload == "c5" and not args.no_weak:
+        del dstates, dwork, out, dbank
+        wplan = shard_plan(rank, world, scaling="weak")
+        wcfg, wbank, wstates, wwork = build_c5(wplan, args.mode)
+        wdb = runtime.DeviceBank(wbank, wcfg.weights, device=device)
+        wds, wdw = wdb.upload_states(wstates), wdb.upload_work(wwork)
+        wout = wdb.alloc_out(wwork, extras=True)
+        wout.tail = None
+        wms, _ = time_device(torch, wdb, wds, wdw, wout, args.steps, args.warmup, flush, world,
+                             device)
+        wmax = reduce_max(wms, world, device)
+        wtot = reduce_sum(float(wwork.n_psi), world, device)
+        weak = {"scaling": "weak", "instances_per_gpu": wplan["count"], "value": wtot / (wmax / 1e3),
+                "unit": UNIT, "ms_per_step": wmax, "psi_per_step": wtot}
 
     c4 = None
-    if world == 1 and args.workload == "c5" and not args.no_c4:
-        c4 = measure_c4(torch, device, args)
+    if args.workload == "c5" and not args.no_c4:
+        c4 = measure_c4(torch, device, args, rank, world)
 
+    items_total = reduce_sum(float(work.n_items), world, device)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (config-5 generator + canonical scenario states, SURVEY §8(d))",
-            "config": {
-                "workload": f"{args.workload}_{args.mode}",
-                "instances_per_gpu": plan["count"] if plan else 1,
-                "stages_per_instance": bank.n_stages // max(1, bank.scalars["n_instances"]),
-                "devices": bank.scalars["n_devices"], "batch": bank.scalars["max_queries"],
-                "horizon": cfg.weights.horizon, "psi_per_gpu_step": work.n_psi,
-                "work_items_per_gpu_step": work.n_items,
-                "l2": "flushed between steps (256 MiB write, outside the events)",
-                "bank_setup_s": round(bank_setup_s, 3),
-                "parallelism": f"dp{world}: "
-                               + ("instances" if args.workload == "c5" else "scenario seeds")
-                               + " sharded by rank, no data-path collective"
-                               + (" + NCCL all-gather of Psi" if args.gather and world > 1
-                                  else ""),
-            },
+            "config": workload_config(args, world),
+            "psi_per_step": psi_total, "work_items_per_step": items_total,
+            "rank0_shard": {k: plan[k] for k in ("first", "count")},
+            "bank_setup_s": round(bank_setup_s, 3),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clocks.summary(),
+            "clocks": csum,
         }
+        if solve is not None:
+            line["host_solve"] = solve
+        if weak is not None:
+            line["weak"] = weak
         if c4 is not None:
             line["c4_sweep"] = c4
-        if host_solve is not None:
-            line["host_solve"] = host_solve
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -609,10 +807,11 @@ def run_fate(args):
     return 0
 
 
-def measure_c4(torch, device, args) -> dict:
+def measure_c4(torch, device, args, rank: int = 0, world: int = 1) -> dict:
     from paper_2605_07238_b200 import pack, runtime
 
-    cfg, bank, states, work = build_c4("sweep")
+    first, n_scen = c4_plan(rank, world)
+    cfg, bank, states, work = build_c4("sweep", n_scen=n_scen, first_scen=first)
     dbank = runtime.DeviceBank(bank, cfg.weights, device=device)
     dstates = dbank.upload_states(states)
     dwork = dbank.upload_work(work)
@@ -621,21 +820,17 @@ def measure_c4(torch, device, args) -> dict:
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)
     clocks = ClockSampler(device.index or 0)
     ms, launches = time_device(torch, dbank, dstates, dwork, out, max(5, args.steps // 4),
-                               min(args.warmup, 3), flush, 1, device, clocks=clocks)
-    nbytes = pack.compulsory_bytes(bank, work, states, dbank.levels,
-                                   runtime.build_windows(bank, dbank.levels))
-    peak, _ = hbm_peak()
-    ach = nbytes / (ms / 1e3) / 1e9
-    return {"workload": "c4_sweep (10k stages x 8 scenarios, 64 devices, 8 models, H=4)",
-            "value": work.n_psi / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
-            "psi_per_step": work.n_psi,
-            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": traffic_for("c4_sweep"),
-                         "bytes_per_launch": nbytes, "bytes_per_candidate": nbytes / work.n_psi,
-                         "issue_ceiling": issue_ceiling(
-                             "c4_sweep", ms, clocks.summary().get("sm_mhz")
-                             or clocks.summary().get("sm_max_mhz"))},
-            "clocks": clocks.summary(), "gpu_launches": launches}
+                               min(args.warmup, 3), flush, world, device, clocks=clocks)
+    ms_max = reduce_max(ms, world, device)
+    tot = reduce_sum(float(work.n_psi), world, device)
+    cs = clocks.summary()
+    return {"workload": "c4_sweep (10k stages x 8 scenarios, 64 devices, 8 models, H=4; "
+                        f"scenarios {C4_SCENARIOS}/{world} per rank)",
+            "value": tot / (ms_max / 1e3), "unit": UNIT, "ms_per_step": ms_max,
+            "psi_per_step": tot,
+            "roofline": _roofline(pack, runtime, bank, work, states, dbank, ms, "c4_sweep",
+                                  cs.get("sm_mhz") or cs.get("sm_max_mhz")),
+            "clocks": cs, "gpu_launches": launches}
 
 
 def main(argv=None):
@@ -646,11 +841,12 @@ def main(argv=None):
     ap.add_argument("--impl", choices=("fate", "reference"), default="fate")
     ap.add_argument("--workload", choices=("c5", "c4"), default="c5")
     ap.add_argument("--mode", choices=("frontier", "sweep"), default="frontier")
-    ap.add_argument("--gather", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-weak", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-instances", type=int, default=16)
+    ap.add_argument("--ref-instances", type=int, default=8)
+    ap.add_argument("--ref-pool", type=int, default=32)
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FATE_ABI_VERSION 2
+#define FATE_ABI_VERSION 3
 #define FATE_MAX_DEVICES 64
 #define FATE_MAX_HORIZON 32
 #define FATE_MAX_QUERIES 256
@@ -211,12 +211,17 @@ typedef struct fate_derived {
 
 /* Outputs.  psi: per item bound(v)*D entries, slot-major, NaN where the
  * device is not eligible; bound(v) = 1 if no_shard else min(R(v), |A(v)|).
- * sched/tail/completion: [W*D], NaN where not eligible; may be NULL. */
+ * sched/tail/completion: [W*D], NaN where not eligible; may be NULL.
+ * timing: [W*D*3] (switch_s, transfer_s, compute_s) of
+ * CostModel.realized_duration(stage, [(d, all queries)]) (costs.py:383-416),
+ * the ShardTiming whose total_s the work-conserving fill compares
+ * (policies.py:91-95); NaN where not eligible; may be NULL. */
 typedef struct fate_out {
     double* psi;
     double* sched;
     double* tail;
     double* completion;
+    double* timing;
 } fate_out;
 
 int fate_abi_version(void);
@@ -292,6 +297,41 @@ typedef struct fate_selection {
 int fate_solve_frontier(const fate_frontier* p, double budget_s, int64_t max_options,
                         fate_selection* out);
 
+/* Host: budget-0 (or budgeted) solves of many independent frontiers straight
+ * from a scored batch -- the per-rank "solve all instances" step of SURVEY
+ * §8(e).  Problem p owns work items [item_ptr[p], item_ptr[p+1]) (one
+ * (instance, scenario) frontier, items in ascending stage order), each with
+ * its bound, eligibility mask and Psi row offset (fate_work.psi_off layout,
+ * HOST copies).  Results: n_sel[p] selected triples at sel[(p*D + k)*3]:
+ * (work item, slot, device), sorted like FrontierSolution.selected;
+ * objective[p], optimal[p].  Problems are spread over n_threads host threads
+ * (<= 0: all hardware threads). */
+typedef struct fate_solve_batch_args {
+    int32_t n_problems;
+    int32_t n_devices;
+    const int32_t* item_ptr;        /* [n_problems+1] */
+    const int32_t* item_bound;      /* [n_items] slots per item */
+    const uint64_t* item_elig;      /* [n_items] eligible-device mask */
+    const int64_t* psi_off;         /* [n_items] */
+    const double* psi;              /* Psi rows (fate_out.psi layout) */
+    double budget_s;
+    int64_t max_options;            /* <= 0: 2^26 */
+    int32_t n_threads;
+    int32_t reserved;
+} fate_solve_batch_args;
+
+typedef struct fate_solve_batch_out {
+    int32_t* n_sel;                 /* [n_problems] */
+    int32_t* sel;                   /* [n_problems*n_devices*3] */
+    double* objective;              /* [n_problems] */
+    int32_t* optimal;               /* [n_problems] */
+    double wall_s;                  /* whole batch */
+    int32_t threads;                /* threads used */
+    int32_t reserved;
+} fate_solve_batch_out;
+
+int fate_solve_batch(const fate_solve_batch_args* a, fate_solve_batch_out* o);
+
 /* ---- device-resident execution-state mirror -----------
  * One running workflow instance's scorer state kept in HBM and updated in
  * place from the executor's transitions (reference state.py:130-272), plus
@@ -328,7 +368,7 @@ int fate_mirror_apply(fate_mirror* m, const fate_event* events, int32_t n_events
                       const int32_t* event_queries, int32_t n_event_queries, void* stream);
 /* The mirror as a one-scenario fate_state (device pointers; scenario 0). */
 int fate_mirror_state(const fate_mirror* m, fate_state* out);
-/* Ready stages (global indices, ascending) into out_dev (device, >= stage
+/* Ready stages (global indices, unordered) into out_dev (device, >= stage
  * count of the instance); *n_out (host) after a stream synchronize.  Reports
  * errors recorded by earlier applies (kappa overflow, bad event). */
 int fate_mirror_ready(fate_mirror* m, int32_t* out_dev, int32_t* n_out, void* stream);
@@ -411,6 +451,10 @@ int fate_pipeline_replay(fate_pipeline* p, void* stream);
 /* Bytes moved host->device and device->host by the last fate_pipeline_score
  * (or captured by fate_pipeline_capture: the bytes of one replay). */
 int fate_pipeline_bytes(const fate_pipeline* p, int64_t* h2d, int64_t* d2h);
+/* The pipeline's device Psi workspace (valid after a run; stable until a
+ * larger batch regrows it): stream-ordered after the replay/score that wrote
+ * it, e.g. for an NCCL all-gather of the per-rank Psi slab. */
+int fate_pipeline_device_psi(const fate_pipeline* p, const double** psi_dev);
 
 #ifdef __cplusplus
 }

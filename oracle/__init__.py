@@ -80,19 +80,21 @@ def score(bank, weights_rec, states, work, n_threads: int = 0, with_extras: bool
     args = HostArgs(bank, weights_rec, states, work)
     n_dev = bank.scalars["n_devices"]
     psi = np.empty(max(work.n_psi, 1), dtype=np.float64)
-    extras = {k: np.empty(max(work.n_items * n_dev, 1), dtype=np.float64)
-              for k in ("sched", "tail", "completion")} if with_extras else {}
+    extras = {k: np.empty(max(work.n_items * n_dev * (3 if k == "timing" else 1), 1),
+                          dtype=np.float64)
+              for k in ("sched", "tail", "completion", "timing")} if with_extras else {}
     out = abi.FateOut(psi=psi.ctypes.data,
                       sched=extras["sched"].ctypes.data if extras else None,
                       tail=extras["tail"].ctypes.data if extras else None,
-                      completion=extras["completion"].ctypes.data if extras else None)
+                      completion=extras["completion"].ctypes.data if extras else None,
+                      timing=extras["timing"].ctypes.data if extras else None)
     rc = lib().oracle_score(C.byref(args.bank), C.byref(args.weights), C.byref(args.state),
                             C.byref(args.work), C.byref(out), int(n_threads))
     if rc != 0:
         raise RuntimeError(f"oracle_score failed: {rc}")
     res = {"psi": psi[: work.n_psi]}
     for k, v in extras.items():
-        res[k] = v[: work.n_items * n_dev]
+        res[k] = v[: work.n_items * n_dev * (3 if k == "timing" else 1)]
     return res
 
 

@@ -75,7 +75,7 @@ class FateDerived(C.Structure):
 
 
 class FateOut(C.Structure):
-    _fields_ = [(n, _p) for n in ("psi", "sched", "tail", "completion")]
+    _fields_ = [(n, _p) for n in ("psi", "sched", "tail", "completion", "timing")]
 
 
 def make_weights(rec: dict) -> FateWeights:

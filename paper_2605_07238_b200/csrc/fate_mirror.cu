@@ -26,7 +26,8 @@
 // Events of a wave are applied in order by one thread (they are few and
 // strictly sequential); the ready set (model.py:306-319) is one thread per
 // stage over the remaining-parent counters plus the claimed flags, compacted
-// in ascending stage index (= sorted(stage_id)).  The mirror's arrays ARE a
+// per warp (ascending within a warp; warps append in completion order, so the
+// set is unordered across warps -- DeviceMirror.ready() sorts it).  The mirror's arrays ARE a
 // one-scenario fate_state: fate_score reads them directly.
 #include <cuda_runtime.h>
 
@@ -213,7 +214,8 @@ __global__ void fate_mirror_apply_kernel(MirrorArgs a, const fate_event* ev, int
 }
 
 // ready_set (model.py:306-319): not completed, not running, not committed,
-// every parent completed -- ascending stage index
+// every parent completed; ascending within each warp's slice, warp slices in
+// completion order (the host sorts)
 __global__ void fate_mirror_ready_kernel(int V, int stage_off, const int32_t* status,
                                          const int32_t* running, const int32_t* remaining,
                                          int32_t* out, int32_t* n_out) {

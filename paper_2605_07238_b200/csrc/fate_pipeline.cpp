@@ -478,4 +478,11 @@ int fate_pipeline_bytes(const fate_pipeline* p, int64_t* h2d, int64_t* d2h) {
     return 0;
 }
 
+int fate_pipeline_device_psi(const fate_pipeline* p, const double** psi_dev) {
+    if (!p || !psi_dev) return fate_internal_fail(FATE_EINVAL, "fate_pipeline_device_psi: NULL");
+    if (!p->psi.p) return fate_internal_fail(FATE_ENOTREADY, "fate_pipeline_device_psi: no run yet");
+    *psi_dev = (const double*)p->psi.p;
+    return 0;
+}
+
 }  // extern "C"

@@ -1011,6 +1011,11 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             if (out.sched) out.sched[orow] = qnan;
             if (out.tail) out.tail[orow] = qnan;
             if (out.completion) out.completion[orow] = qnan;
+            if (out.timing) {
+                out.timing[3 * orow + 0] = qnan;
+                out.timing[3 * orow + 1] = qnan;
+                out.timing[3 * orow + 2] = qnan;
+            }
             continue;
         }
         const double wait = py_max0(V6_PICK(fr) - clock);
@@ -1104,6 +1109,11 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         if (out.sched) out.sched[orow] = S;
         if (out.tail) out.tail[orow] = tail_j;
         if (out.completion) out.completion[orow] = wait + full_total;
+        if (out.timing) {  // ShardTiming(switch_s, transfer_s, compute_s), costs.py:398-414
+            out.timing[3 * orow + 0] = sw;
+            out.timing[3 * orow + 1] = tr;
+            out.timing[3 * orow + 2] = here_j;
+        }
         psi[d] = S + tail_j;
 
         // _marginal_shard_score (costs.py:249-279)

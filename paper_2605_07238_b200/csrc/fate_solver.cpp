@@ -29,7 +29,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <atomic>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -376,6 +378,84 @@ int fate_solve_frontier(const fate_frontier* p, double budget_s, int64_t max_opt
     for (const Stage& G : S.st) out->n_options += (int64_t)G.opts.size();
     out->wall_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return 0;
+}
+
+// Many independent problems straight from a scored batch (one problem =
+// one (instance, scenario) frontier, its work items consecutive and in
+// stage order): each problem's CSR rows are rebuilt from the dense Psi rows
+// (eligible devices ascending) and solved exactly like fate_solve_frontier,
+// problems distributed over host threads.
+int fate_solve_batch(const fate_solve_batch_args* a, fate_solve_batch_out* o) {
+    if (!a || !o || !a->item_ptr || !a->item_bound || !a->item_elig || !a->psi_off || !a->psi ||
+        !o->n_sel || !o->sel || !o->objective || !o->optimal)
+        return fate_internal_fail(FATE_EINVAL, "fate_solve_batch: NULL argument");
+    const int D = a->n_devices;
+    if (a->n_problems < 0 || D < 1 || D > FATE_MAX_DEVICES)
+        return fate_internal_fail(FATE_EINVAL, "fate_solve_batch: bad sizes");
+    int nt = a->n_threads > 0 ? a->n_threads : (int)std::thread::hardware_concurrency();
+    nt = std::max(1, std::min(nt, std::max(1, a->n_problems)));
+    std::atomic<int> next{0};
+    std::atomic<int> status{0};
+    std::string first_error;
+    std::atomic<bool> have_error{false};
+    auto work = [&]() {
+        std::vector<int32_t> slot_ptr, cand_ptr, cand_dev, st, sl, dv;
+        std::vector<double> cand_psi;
+        st.resize(D);
+        sl.resize(D);
+        dv.resize(D);
+        for (;;) {
+            const int p = next.fetch_add(1);
+            if (p >= a->n_problems || status.load() != 0) return;
+            slot_ptr.assign(1, 0);
+            cand_ptr.assign(1, 0);
+            cand_dev.clear();
+            cand_psi.clear();
+            const int i0 = a->item_ptr[p], i1 = a->item_ptr[p + 1];
+            for (int i = i0; i < i1; ++i) {
+                const uint64_t m = a->item_elig[i];
+                for (int k = 0; k < a->item_bound[i]; ++k) {
+                    const double* row = a->psi + a->psi_off[i] + (int64_t)k * D;
+                    for (int d = 0; d < D; ++d)
+                        if ((m >> d) & 1ull) {
+                            cand_dev.push_back(d);
+                            cand_psi.push_back(row[d]);
+                        }
+                    cand_ptr.push_back((int32_t)cand_dev.size());
+                }
+                slot_ptr.push_back((int32_t)cand_ptr.size() - 1);
+            }
+            fate_frontier fr{i1 - i0, D, slot_ptr.data(), cand_ptr.data(), cand_dev.data(),
+                             cand_psi.data()};
+            fate_selection out{D, 0, st.data(), sl.data(), dv.data(), 0.0, 0, 0, 0, 0, 0.0};
+            const int rc = fate_solve_frontier(&fr, a->budget_s, a->max_options, &out);
+            if (rc) {
+                bool expect = false;
+                if (have_error.compare_exchange_strong(expect, true))
+                    first_error = fate_last_error();
+                status.store(rc);
+                return;
+            }
+            o->n_sel[p] = out.n;
+            for (int k = 0; k < out.n; ++k) {
+                int32_t* t = o->sel + ((int64_t)p * D + k) * 3;
+                t[0] = i0 + out.stage[k];  // work item of the selected stage
+                t[1] = out.slot[k];
+                t[2] = out.device[k];
+            }
+            o->objective[p] = out.objective;
+            o->optimal[p] = out.optimal;
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    o->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    o->threads = nt;
+    if (status.load() != 0) return fate_internal_fail(status.load(), first_error);
     return 0;
 }
 

@@ -8,7 +8,8 @@ live state's transitions (``commit_stage``, ``on_task_start``,
 ``on_task_complete``; reference ``state.py:130-181``) as events, applies them
 on the device once per wave, and hands ``fate_score`` the mirror itself as its
 one-scenario ``fate_state``.  :class:`MirrorScorer` is a drop-in for
-``planner.GpuScorer`` that scores from the mirror.
+``planner.GpuScorer`` that scores from the mirror; ``compat.install(mirror=...)``
+hooks it into the unchanged reference executor.
 """
 
 from __future__ import annotations
@@ -18,7 +19,7 @@ import ctypes as C
 import numpy as np
 
 from . import abi, pack
-from .planner import GpuScorer, WaveScores
+from .planner import GpuScorer, WaveScores, wave_scores
 from .runtime import DeviceBank, _check, load_library
 
 EV_COMMIT, EV_START, EV_COMPLETE = 0, 1, 2
@@ -140,7 +141,8 @@ class DeviceMirror:
         n = C.c_int32(0)
         _check(self.L.fate_mirror_ready(self.handle, C.c_void_p(self._ready.data_ptr()),
                                         C.byref(n), C.c_void_p(s.cuda_stream)), "fate_mirror_ready")
-        idx = self._ready[: n.value].cpu().numpy()
+        # the kernel compacts per warp in completion order; ids ascend after a sort
+        idx = np.sort(self._ready[: n.value].cpu().numpy())
         return [self.stage_ids[int(g) - self.goff] for g in idx]
 
     def download(self) -> dict:
@@ -184,37 +186,55 @@ def _device_view(torch, ptr: int, count: int, typestr: str) -> np.ndarray:
 class MirrorScorer(GpuScorer):
     """``GpuScorer`` drop-in that scores from the device-resident mirror of the
     running instance instead of packing the per-wave snapshot.  Pass it both as
-    the policy's scorer and as ``simulate.run(..., observer=scorer)``."""
+    the policy's scorer and to ``compat.install(mirror=scorer)``, which attaches
+    the reference executor's live state to it."""
 
     def __init__(self, device=None, kappa_cap: int = 16, check_ready: bool = False,
                  gpu_frontier: bool = False):
         """``check_ready``: assert the GPU ready set equals the executor's
         frontier every wave.  ``gpu_frontier``: the executor takes each wave's
-        frontier from the GPU ready set (``frontier()``)."""
+        frontier from the GPU ready set (``frontier()``) once the mirror exists
+        (from the first scored wave on)."""
         super().__init__(device=device)
         self.kappa_cap = kappa_cap
         self.check_ready = check_ready
         self.provides_frontier = gpu_frontier
         self.mirror: DeviceMirror | None = None
         self._instance = None
+        self._live = None
         self.ready_checks = 0
+        self.gpu_frontiers = 0
 
-    def attach(self, state, cost_model) -> None:
-        dbank = self.bank_for(state.instance, cost_model.models, cost_model.topo,
-                              cost_model.weights)
+    def attach_live(self, state) -> None:
+        """Follow a live executor state.  The device mirror is created at the
+        first scored wave (when the catalog is known); the executor commits
+        nothing before its first wave, so no transition is missed."""
         if self.mirror is not None:
             self.mirror.close()
-        self.mirror = DeviceMirror(dbank, 0, self.kappa_cap)
-        self.mirror.attach(state)
+            self.mirror = None
+        self._live = state
         self._instance = state.instance
 
-    def frontier(self) -> list:
+    def _ensure_mirror(self, cost_model) -> None:
+        if self.mirror is None and self._live is not None:
+            dbank = self.bank_for(self._instance, cost_model.models, cost_model.topo,
+                                  cost_model.weights)
+            self.mirror = DeviceMirror(dbank, 0, self.kappa_cap)
+            self.mirror.attach(self._live)
+
+    def follows(self, dag) -> bool:
+        return self.mirror is not None and self._instance is not None and \
+            self._instance.dag is dag
+
+    def frontier(self) -> set:
         """The next wave's frontier: the GPU ready set (model.py:306-319)."""
-        return self.mirror.ready()
+        self.gpu_frontiers += 1
+        return set(self.mirror.ready())
 
     def score_wave(self, frontier, state, cost_model, dag=None) -> WaveScores:
-        if self.mirror is None or state.instance is not self._instance:
+        if self._live is None or state.instance is not self._instance:
             return super().score_wave(frontier, state, cost_model, dag)
+        self._ensure_mirror(cost_model)
         dbank = self.mirror.dbank
         packed = dbank.packed
         m = self.mirror
@@ -228,19 +248,10 @@ class MirrorScorer(GpuScorer):
         work = pack.make_work(packed, [(0, packed.global_index(0, s)) for s in sids],
                               dbank.no_shard)
         dwork = dbank.upload_work(work)
-        out = dbank.alloc_out(work, extras=True)
+        out = dbank.alloc_out(work, extras=True, timing=True)
 
         class _S:
             cstate = m.cstate
 
         res = dbank.score_into(_S, dwork, out)
-        D = packed.scalars["n_devices"]
-        n = len(sids)
-        host = {k: getattr(res, k).cpu().numpy() for k in ("psi", "sched", "completion", "tail")}
-        return WaveScores(
-            stage_ids=sids, bounds=[int(b) for b in work.bounds], device_ids=packed.device_ids,
-            elig=[int(packed.arrays["st_elig"][g]) for g in work.stage],
-            psi=host["psi"][: work.n_psi], psi_off=work.psi_off,
-            sched=host["sched"][: n * D].reshape(n, D),
-            completion=host["completion"][: n * D].reshape(n, D),
-            tail=host["tail"][: n * D].reshape(n, D))
+        return wave_scores(packed, sids, work, res)

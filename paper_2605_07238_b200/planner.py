@@ -1,16 +1,27 @@
-"""Drop-in GPU cost matrix and the FATE policy that consumes it.
+"""Drop-in GPU cost matrix for the reference scheduler, and the FATE policy
+that consumes it.
 
-* :func:`build_problem` -- same signature and result as the reference
+This module sits *behind* the caller's own ``wfsched`` (the reference
+package): every type it returns is the caller's type and every decision
+that is not scoring is the caller's code.
+
+* :func:`build_problem` -- same signature and result as
   ``wfsched.planner.build_problem(frontier, state, cost_model, dag)``
-  (``pkg/src/wfsched/planner.py:75-98``): one ``Candidate`` per
-  (sorted stage, slot < bound, sorted eligible device), Psi bit-identical,
-  negative scores retained -- computed by the sm_100a kernel.
-* :class:`FateGpuPolicy` -- the reference ``FatePolicy`` (``policies.py:44-193``,
-  ``name = "fate"``) with its three scorer consumers on the GPU: the cost
-  matrix, the horizon-0 greedy S matrix (``policies.py:129-150``) and the
-  work-conserving completion matrix (``policies.py:79-127``).  The frontier
-  solve stays on the host (:func:`.wf.frontier.solve_frontier`) and is timed
-  separately in ``solver_stats``.
+  (``pkg/src/wfsched/planner.py:75-98``): a ``wfsched.planner.FrontierProblem``
+  of ``wfsched.planner.Candidate`` (sorted stage, slot < bound, sorted eligible
+  device), Psi bit-identical, negative scores retained -- computed by the
+  sm_100a kernel in one launch per wave.
+* :class:`WaveCostModel` -- a read-only view of ``wfsched.costs.CostModel``
+  answering ``plan_score`` / ``sched_score`` / ``tail_value`` and the
+  full-batch ``realized_duration`` (``costs.py:210-247, 281-352, 383-416``)
+  from one GPU-scored wave.
+* :class:`FateGpuPolicy` -- a subclass of the caller's
+  ``wfsched.policies.FatePolicy`` (``policies.py:44-193``, ``name = "fate"``).
+  It scores the wave on the GPU and hands the caller's own methods the view:
+  the horizon-0 greedy (``_greedy_wave``, reads S), the work-conserving fill
+  (``_extend_work_conserving``, reads ``realized_duration``), ``_materialize`` /
+  ``_align_shards`` and the solve (``wfsched.planner.solve_frontier``, or the
+  native restatement ``solver="native"``) all run unchanged, host-side.
 
 No CPU fallback: without CUDA or ``libfate.so`` these raise
 :class:`~paper_2605_07238_b200.runtime.FateUnavailable`.
@@ -18,6 +29,7 @@ No CPU fallback: without CUDA or ``libfate.so`` these raise
 
 from __future__ import annotations
 
+import importlib
 import time
 from collections import OrderedDict
 from dataclasses import dataclass
@@ -26,8 +38,20 @@ import numpy as np
 
 from . import pack
 from .runtime import DeviceBank
-from .wf.frontier import Candidate, FrontierProblem, SolverStats, solve_frontier
-from .wf.simulate import ScheduledTask, partition_shards
+
+
+def _wf(name: str):
+    """A module of the caller's ``wfsched`` (the package this is a drop-in for)."""
+    try:
+        return importlib.import_module(f"wfsched.{name}")
+    except ImportError as exc:  # pragma: no cover - depends on the caller
+        raise ImportError("paper_2605_07238_b200.planner plugs into the reference scheduler "
+                          "package 'wfsched'; make it importable") from exc
+
+
+_PLANNER = _wf("planner")
+_POLICIES = _wf("policies")
+_COSTS = _wf("costs")
 
 
 @dataclass
@@ -43,8 +67,11 @@ class WaveScores:
     sched: np.ndarray    # [F, D]
     completion: np.ndarray
     tail: np.ndarray
+    timing: np.ndarray | None = None  # [F, D, 3] switch, transfer, compute
 
     def candidates(self):
+        """``wfsched.planner.Candidate`` tuples in ``build_problem`` order."""
+        Candidate = _PLANNER.Candidate
         out = []
         D = len(self.device_ids)
         for i, sid in enumerate(self.stage_ids):
@@ -90,17 +117,24 @@ class GpuScorer:
         states = pack.pack_states(packed, [(0, state)])
         work = pack.make_work(packed, [(0, packed.global_index(0, s)) for s in sids],
                               dbank.no_shard)
-        res = dbank.score(states, work, extras=True)
-        D = packed.scalars["n_devices"]
-        n = len(sids)
-        host = {k: getattr(res, k).cpu().numpy() for k in ("psi", "sched", "completion", "tail")}
-        return WaveScores(
-            stage_ids=sids, bounds=[int(b) for b in work.bounds], device_ids=packed.device_ids,
-            elig=[int(packed.arrays["st_elig"][g]) for g in work.stage],
-            psi=host["psi"][: work.n_psi], psi_off=work.psi_off,
-            sched=host["sched"][: n * D].reshape(n, D),
-            completion=host["completion"][: n * D].reshape(n, D),
-            tail=host["tail"][: n * D].reshape(n, D))
+        res = dbank.score(states, work, extras=True, timing=True)
+        return wave_scores(packed, sids, work, res)
+
+
+def wave_scores(packed, sids, work, res) -> WaveScores:
+    """Host copies of a scored wave (one D2H per output)."""
+    D = packed.scalars["n_devices"]
+    n = len(sids)
+    host = {k: getattr(res, k).cpu().numpy() for k in ("psi", "sched", "completion", "tail")}
+    timing = res.timing.cpu().numpy()[: n * D * 3].reshape(n, D, 3) if res.timing is not None \
+        else None
+    return WaveScores(
+        stage_ids=sids, bounds=[int(b) for b in work.bounds], device_ids=packed.device_ids,
+        elig=[int(packed.arrays["st_elig"][g]) for g in work.stage],
+        psi=host["psi"][: work.n_psi], psi_off=work.psi_off,
+        sched=host["sched"][: n * D].reshape(n, D),
+        completion=host["completion"][: n * D].reshape(n, D),
+        tail=host["tail"][: n * D].reshape(n, D), timing=timing)
 
 
 _DEFAULT_SCORER: GpuScorer | None = None
@@ -116,31 +150,91 @@ def default_scorer() -> GpuScorer:
 def build_problem(frontier, state, cost_model, dag, scorer: GpuScorer | None = None):
     """GPU replacement of ``wfsched.planner.build_problem`` (planner.py:75-98)."""
     wave = (scorer or default_scorer()).score_wave(frontier, state, cost_model, dag)
-    return _problem_of(wave, cost_model)
+    return problem_of(wave, cost_model)
 
 
-def _problem_of(wave: WaveScores, cost_model) -> FrontierProblem:
-    return FrontierProblem(candidates=tuple(wave.candidates()),
-                           shard_bounds=dict(zip(wave.stage_ids, wave.bounds)),
-                           device_ids=tuple(cost_model.topo.device_ids))
+def problem_of(wave: WaveScores, cost_model):
+    """The caller's ``FrontierProblem`` of a scored wave (planner.py:93-98)."""
+    return _PLANNER.FrontierProblem(candidates=tuple(wave.candidates()),
+                                    shard_bounds=dict(zip(wave.stage_ids, wave.bounds)),
+                                    device_ids=cost_model.topo.device_ids)
 
 
-class FateGpuPolicy:
-    """Frontier planning with GPU horizon-aware scores (reference
-    policies.py:44-193); drop-in for ``make_policy("fate")``."""
+class WaveCostModel:
+    """``wfsched.costs.CostModel`` answering from one GPU-scored wave.
+
+    Everything the FATE policy asks its cost model about a wave -- Psi
+    (``plan_score``), S (``sched_score``), the tail (``tail_value``) and the
+    full-batch ``realized_duration`` -- comes from the GPU outputs of that
+    wave; the catalog attributes (``models``, ``topo``, ``weights``) are the
+    wrapped model's.  Contract violations raise the reference's ``ValueError``
+    (``costs.py:152-153, 242-243, 391-401``); anything the wave did not score
+    raises ``KeyError`` instead of silently computing it on the CPU."""
+
+    def __init__(self, cost_model, wave: WaveScores, state):
+        self._cm = cost_model
+        self._wave = wave
+        self._state = state
+        self._row = {sid: i for i, sid in enumerate(wave.stage_ids)}
+        self._col = {dev: j for j, dev in enumerate(wave.device_ids)}
+        self._queries = tuple(q.query_id for q in state.instance.queries)
+
+    def __getattr__(self, name):
+        return getattr(self._cm, name)
+
+    def _cell(self, stage, device_id: str, state):
+        if state is not self._state:
+            raise KeyError("WaveCostModel answers only for the state its wave was scored on")
+        if device_id not in stage.eligible_devices:
+            raise ValueError(f"device {device_id} not eligible for stage {stage.id}")
+        return self._row[stage.id], self._col[device_id]
+
+    def plan_score(self, stage, slot: int, device_id: str, state, dag) -> float:
+        if slot >= stage.shard_bound:
+            raise ValueError(f"slot {slot} exceeds shard bound of stage {stage.id}")
+        i, j = self._cell(stage, device_id, state)
+        w = self._wave
+        if slot >= w.bounds[i]:
+            raise KeyError(f"slot {slot} of {stage.id} was not scored")
+        return float(w.psi[int(w.psi_off[i]) + slot * len(w.device_ids) + j])
+
+    def sched_score(self, stage, device_id: str, state, dag) -> float:
+        i, j = self._cell(stage, device_id, state)
+        return float(self._wave.sched[i, j])
+
+    def tail_value(self, stage, device_id: str, state, dag) -> float:
+        if self._cm.weights.effective_horizon() <= 1:
+            return 0.0
+        i, j = self._cell(stage, device_id, state)
+        return float(self._wave.tail[i, j])
+
+    def realized_duration(self, stage, shard_assignment, state, dag=None):
+        """Full-batch single-shard timing from the wave (the work-conserving
+        fill's only use, policies.py:91-95)."""
+        if len(shard_assignment) != 1 or tuple(shard_assignment[0][1]) != self._queries:
+            raise KeyError("the wave holds full-batch single-shard timings only")
+        device_id = shard_assignment[0][0]
+        i, j = self._cell(stage, device_id, state)
+        sw, tr, comp = (float(x) for x in self._wave.timing[i, j])
+        return [_COSTS.ShardTiming(device_id=device_id, queries=self._queries, switch_s=sw,
+                                   transfer_s=tr, compute_s=comp)]
+
+
+class FateGpuPolicy(_POLICIES.FatePolicy):
+    """The caller's ``FatePolicy`` (policies.py:44-193) with its scorer on the
+    GPU; drop-in for ``make_policy("fate")``.
+
+    ``solver``: "reference" = the caller's ``wfsched.planner.solve_frontier``
+    (default), "native" = ``fate_solve_frontier`` (same result whenever both
+    finish and at a zero budget; finishes more problems inside a budget)."""
 
     name = "fate"
 
     def __init__(self, solver_budget_s: float = 0.25, scorer: GpuScorer | None = None,
-                 solver: str = "python"):
-        """``solver``: "python" = the restated reference solve (default: its
-        wall-clock behaviour matches the reference's), "native" =
-        ``fate_solve_frontier`` (same result whenever both finish or at a zero
-        budget; finishes more problems within a budget)."""
-        if solver not in ("python", "native"):
+                 solver: str = "reference"):
+        if solver not in ("reference", "native"):
             raise ValueError(f"unknown solver {solver!r}")
-        self.solver_budget_s = solver_budget_s
-        self.solver_stats = SolverStats()
+        super().__init__(solver_budget_s=solver_budget_s)
         self.scorer = scorer or default_scorer()
         self.score_seconds = 0.0
         self.solver = solver
@@ -149,108 +243,24 @@ class FateGpuPolicy:
 
             self._solve = native
         else:
-            self._solve = solve_frontier
+            self._solve = _PLANNER.solve_frontier
 
     def plan_wave(self, state, frontier, dag, cost_model) -> list:
+        """``FatePolicy.plan_wave`` (policies.py:53-76) on one GPU launch."""
         t0 = time.perf_counter()
         wave = self.scorer.score_wave(frontier, state, cost_model, dag)
         self.score_seconds += time.perf_counter() - t0
-        queries = tuple(q.query_id for q in state.instance.queries)
+        view = WaveCostModel(cost_model, wave, state)
         if cost_model.weights.horizon == 0:
-            return self._greedy_wave(wave, queries)
-        problem = _problem_of(wave, cost_model)
+            return self._greedy_wave(state, frontier, dag, view)
+        problem = problem_of(wave, cost_model)
         solution = self._solve(problem, budget_s=self.solver_budget_s)
         self.solver_stats.record(solution)
-        chosen = self._fill_idle(solution.selected, problem, wave, state)
-        if not chosen:
+        selected = self._extend_work_conserving(solution.selected, problem, state, dag, view)
+        if not selected:
             if state.running_tasks:
                 return []
-            top = min((c for c in problem.candidates if c.slot == 0),
-                      key=lambda c: (-c.psi, c.stage_id, c.device_id))
-            chosen = ((top.stage_id, 0, top.device_id),)
-        return self._materialize(chosen, state, dag, queries)
-
-    @staticmethod
-    def _fill_idle(selected, problem, wave: WaveScores, state):
-        """``_extend_work_conserving`` (policies.py:79-127) on the GPU
-        completion matrix: wait + realized full-batch duration per (v, d)."""
-        row = {sid: i for i, sid in enumerate(wave.stage_ids)}
-        col = {dev: j for j, dev in enumerate(wave.device_ids)}
-        done = wave.completion
-        chosen = list(selected)
-        used = {d for _, _, d in chosen}
-        taken = {s for s, _, _ in chosen}
-        idle = {d for d, free in state.device_free.items()
-                if free <= state.clock + 1e-12 and d not in used}
-        while idle:
-            pool = [c for c in problem.candidates
-                    if c.slot == 0 and c.device_id in idle and c.stage_id not in taken]
-            if not pool:
-                break
-            pick = None
-            for c in sorted(pool, key=lambda c: (-c.psi, c.stage_id, c.device_id)):
-                i = row[c.stage_id]
-                m = wave.elig[i]
-                elsewhere = min(float(done[i, j]) for j in range(len(wave.device_ids)) if m >> j & 1)
-                if float(done[i, col[c.device_id]]) <= elsewhere + 1e-9:
-                    pick = c
-                    break
-            if pick is None:
-                break
-            chosen.append((pick.stage_id, 0, pick.device_id))
-            idle.discard(pick.device_id)
-            taken.add(pick.stage_id)
-        return tuple(sorted(chosen))
-
-    @staticmethod
-    def _greedy_wave(wave: WaveScores, queries) -> list:
-        """Horizon 0: myopic placement by the GPU S matrix (policies.py:129-150)."""
-        ranked = []
-        for i, sid in enumerate(wave.stage_ids):
-            m = wave.elig[i]
-            for j, dev in enumerate(wave.device_ids):
-                if m >> j & 1:
-                    ranked.append((-float(wave.sched[i, j]), sid, dev))
-        ranked.sort()
-        used: set = set()
-        placed: dict = {}
-        for _, sid, dev in ranked:
-            if sid in placed or dev in used:
-                continue
-            placed[sid] = dev
-            used.add(dev)
-        return [ScheduledTask(task_id="", stage_id=s, slot=0, device_id=d, queries=queries)
-                for s, d in sorted(placed.items())]
-
-    def _materialize(self, chosen, state, dag, queries) -> list:
-        by_stage: dict = {}
-        for sid, k, dev in chosen:
-            by_stage.setdefault(sid, []).append((k, dev))
-        tasks = []
-        for sid in sorted(by_stage):
-            stage = dag.stages[sid]
-            devs = [d for _, d in sorted(by_stage[sid])]
-            devs = self._align(stage, devs, queries, state)
-            tasks.extend(ScheduledTask(task_id="", stage_id=sid, slot=k, device_id=dev,
-                                       queries=shard)
-                         for k, (dev, shard) in enumerate(partition_shards(stage, devs, queries)))
-        return tasks
-
-    @staticmethod
-    def _align(stage, devs, queries, state) -> list:
-        """Swap a 2-way split when that keeps more cached query prefix local
-        (policies.py:174-193)."""
-        if len(devs) != 2:
-            return devs
-        halves = partition_shards(stage, devs, queries)
-
-        def kept(qids, dev) -> int:
-            tot = 0
-            for qid in qids:
-                q = state.query(qid)
-                tot += min(state.cached_tokens(dev, q.prefix_group, stage.model), q.prompt_tokens)
-            return tot
-
-        same = kept(halves[0][1], devs[0]) + kept(halves[1][1], devs[1])
-        swap = kept(halves[0][1], devs[1]) + kept(halves[1][1], devs[0])
-        return [devs[1], devs[0]] if swap > same else devs
+            best = min((c for c in problem.candidates if c.slot == 0),
+                       key=lambda c: (-c.psi, c.stage_id, c.device_id))
+            selected = ((best.stage_id, 0, best.device_id),)
+        return self._materialize(selected, state, dag)

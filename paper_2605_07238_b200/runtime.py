@@ -72,7 +72,9 @@ def load_library():
     L.fate_pipeline_replay.argtypes = [C.c_void_p, C.c_void_p]
     L.fate_pipeline_bytes.restype = C.c_int
     L.fate_pipeline_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
-    if L.fate_abi_version() != 2:
+    L.fate_pipeline_device_psi.restype = C.c_int
+    L.fate_pipeline_device_psi.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    if L.fate_abi_version() != 3:
         raise FateUnavailable("libfate.so ABI version mismatch")
     _lib = L
     return L
@@ -200,6 +202,7 @@ class ScoreResult:
     sched: object        # torch float64 [W*D] or None
     tail: object
     completion: object
+    timing: object = None  # torch float64 [W*D*3] (switch, transfer, compute) or None
 
 
 class DeviceBank:
@@ -298,13 +301,14 @@ class DeviceBank:
     def upload_work(self, work: WorkList, non_blocking: bool = False) -> "DeviceWork":
         return DeviceWork(self, work, non_blocking=non_blocking)
 
-    def alloc_out(self, work: WorkList, extras: bool = True) -> ScoreResult:
+    def alloc_out(self, work: WorkList, extras: bool = True, timing: bool = False) -> ScoreResult:
         torch = self.torch
         n_dev = self.packed.scalars["n_devices"]
         f64 = dict(dtype=torch.float64, device=self.device)
         psi = torch.empty(max(work.n_psi, 1), **f64)
         mk = (lambda: torch.empty(max(work.n_items * n_dev, 1), **f64)) if extras else (lambda: None)
-        return ScoreResult(psi=psi, sched=mk(), tail=mk(), completion=mk())
+        tm = torch.empty(max(work.n_items * n_dev * 3, 1), **f64) if timing else None
+        return ScoreResult(psi=psi, sched=mk(), tail=mk(), completion=mk(), timing=tm)
 
     def score_into(self, dstates: "DeviceStates", dwork: "DeviceWork", out: ScoreResult,
                    stream=None) -> ScoreResult:
@@ -314,17 +318,19 @@ class DeviceBank:
             psi=out.psi.data_ptr(),
             sched=out.sched.data_ptr() if out.sched is not None else None,
             tail=out.tail.data_ptr() if out.tail is not None else None,
-            completion=out.completion.data_ptr() if out.completion is not None else None)
+            completion=out.completion.data_ptr() if out.completion is not None else None,
+            timing=out.timing.data_ptr() if out.timing is not None else None)
         _check(load_library().fate_score(
             C.byref(self.cbank), C.byref(self.cweights), C.byref(self.cwin), C.byref(self.cder),
             C.byref(dstates.cstate), C.byref(dwork.cwork), C.byref(cout),
             C.c_void_p(s.cuda_stream)), "fate_score")
         return out
 
-    def score(self, states: PackedStates, work: WorkList, extras: bool = True) -> ScoreResult:
+    def score(self, states: PackedStates, work: WorkList, extras: bool = True,
+              timing: bool = False) -> ScoreResult:
         ds = self.upload_states(states)
         dw = self.upload_work(work)
-        out = self.alloc_out(work, extras)
+        out = self.alloc_out(work, extras, timing)
         return self.score_into(ds, dw, out)
 
 
@@ -428,6 +434,20 @@ class HostPipeline:
             ptr(self.host_sched), ptr(self.host_completion), C.c_void_p(s.cuda_stream)),
             "fate_pipeline_score")
         return self.host_psi
+
+    def device_psi(self):
+        """The pipeline's device Psi rows as a torch tensor view (no copy)."""
+        torch = self.dbank.torch
+        ptr = C.c_void_p()
+        _check(self.L.fate_pipeline_device_psi(self.handle, C.byref(ptr)),
+               "fate_pipeline_device_psi")
+        n = max(int(self.batch.n_psi), 1)
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                        "data": (int(ptr.value), False), "version": 3}
+
+        return torch.as_tensor(_View(), device=self.dbank.device)
 
     def close(self):
         if getattr(self, "handle", None):

@@ -17,8 +17,8 @@ completed on hashed devices (2-way sharded when hashed so), their prefix
 entries seeded exactly as the reference's ``_seed_prefixes`` would
 (``state.py:236-261``), then each device gets a hashed resident model (with the
 reference eviction rule, ``state.py:224-234``) and a hashed free time.  It is
-written against a small "kit" of state primitives so the same function builds
-reference-side states (golden generation) and mirror-side states (GPU box).
+written against a small "kit" of state primitives (by default the caller's
+``wfsched``: the states are real reference ``ExecutionState`` objects).
 """
 
 from __future__ import annotations
@@ -40,11 +40,14 @@ class StateKit:
     partition_shards: object  # executor.partition_shards
 
 
-def mirror_kit() -> StateKit:
-    from .wf.execstate import ExecutionState, PrefixEntry, merge_prefix_entry
-    from .wf.simulate import partition_shards
+def reference_kit() -> StateKit:
+    """The caller's ``wfsched`` state primitives (``state.py:26-272``,
+    ``executor.py:86-108``)."""
+    from wfsched.executor import partition_shards
+    from wfsched.state import ExecutionState, PrefixEntry
 
-    return StateKit(ExecutionState.initial, PrefixEntry, merge_prefix_entry, partition_shards)
+    return StateKit(ExecutionState.initial, PrefixEntry, ExecutionState._merge_entry,
+                    partition_shards)
 
 
 # ---------------------------------------------------------------------------
@@ -95,7 +98,7 @@ def c5_instance(i: int, cfg=None):
 
 def build_scenario(instance, cfg, s: int, kit: StateKit | None = None):
     """Deterministic mid-run state for scenario seed ``s``."""
-    kit = kit or mirror_kit()
+    kit = kit or reference_kit()
     dag = instance.dag
     devs = sorted(cfg.topology.device_ids)
     n_dev = len(devs)

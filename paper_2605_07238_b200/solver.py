@@ -1,7 +1,7 @@
 """Native host frontier solve (``fate_solve_frontier``), drop-in for
 ``wfsched.planner.solve_frontier`` (reference ``pkg/src/wfsched/planner.py:150-214``).
 
-Same signature, same :class:`~.wf.frontier.FrontierSolution` (selection,
+Same signature, the caller's ``wfsched.planner.FrontierSolution`` (selection,
 objective bits, ``optimal`` flag, ``nodes_explored``); the option enumeration,
 memoised search, tie-break and greedy fallback run in C++
 (``csrc/fate_solver.cpp``).  Only ``wall_time`` -- and therefore which
@@ -17,7 +17,6 @@ import ctypes as C
 import numpy as np
 
 from .runtime import _check, load_library
-from .wf.frontier import FrontierProblem, FrontierSolution
 
 
 class _Frontier(C.Structure):
@@ -42,7 +41,7 @@ def _lib():
     return L
 
 
-def pack_problem(problem: FrontierProblem):
+def pack_problem(problem):
     """FrontierProblem -> (stage ids, device ids, CSR arrays) in the order the
     reference's ``_stage_options`` visits them."""
     devices = sorted(set(problem.device_ids))
@@ -70,8 +69,10 @@ def pack_problem(problem: FrontierProblem):
     return stages, devices, arrays
 
 
-def solve_frontier(problem: FrontierProblem, budget_s: float = 0.25,
-                   max_options: int = 0) -> FrontierSolution:
+def solve_frontier(problem, budget_s: float = 0.25, max_options: int = 0):
+    """``wfsched.planner.solve_frontier`` (planner.py:150-214) natively."""
+    from wfsched.planner import FrontierSolution
+
     if not problem.candidates:
         raise ValueError("solve_frontier requires a nonempty problem")
     L = _lib()
@@ -91,3 +92,58 @@ def solve_frontier(problem: FrontierProblem, budget_s: float = 0.25,
     return FrontierSolution(selected=sel, objective=float(out.objective),
                             optimal=bool(out.optimal), wall_time=float(out.wall_s),
                             nodes_explored=int(out.nodes))
+
+
+class _BatchArgs(C.Structure):
+    _fields_ = [("n_problems", C.c_int32), ("n_devices", C.c_int32), ("item_ptr", C.c_void_p),
+                ("item_bound", C.c_void_p), ("item_elig", C.c_void_p), ("psi_off", C.c_void_p),
+                ("psi", C.c_void_p), ("budget_s", C.c_double), ("max_options", C.c_int64),
+                ("n_threads", C.c_int32), ("reserved", C.c_int32)]
+
+
+class _BatchOut(C.Structure):
+    _fields_ = [("n_sel", C.c_void_p), ("sel", C.c_void_p), ("objective", C.c_void_p),
+                ("optimal", C.c_void_p), ("wall_s", C.c_double), ("threads", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class BatchSolution:
+    """Per problem: selected (work item, slot, device) triples, objective,
+    optimal flag; plus the batch's wall time and thread count."""
+
+    def __init__(self, n_sel, sel, objective, optimal, wall_s, threads):
+        self.n_sel, self.sel, self.objective, self.optimal = n_sel, sel, objective, optimal
+        self.wall_s, self.threads = wall_s, threads
+
+    def selected(self, p: int) -> np.ndarray:
+        return self.sel[p, : self.n_sel[p]]
+
+
+def solve_batch(item_ptr, item_bound, item_elig, psi_off, psi, n_devices: int,
+                budget_s: float = 0.0, n_threads: int = 0, max_options: int = 0) -> BatchSolution:
+    """``fate_solve_batch``: every problem of a scored batch solved on host
+    threads (problem p = work items ``item_ptr[p]:item_ptr[p+1]``, in stage
+    order; ``psi`` the host copy of the batch's Psi rows)."""
+    L = load_library()
+    if not getattr(L, "_batch_bound", False):
+        L.fate_solve_batch.restype = C.c_int
+        L.fate_solve_batch.argtypes = [C.POINTER(_BatchArgs), C.POINTER(_BatchOut)]
+        L._batch_bound = True
+    item_ptr = np.ascontiguousarray(item_ptr, dtype=np.int32)
+    item_bound = np.ascontiguousarray(item_bound, dtype=np.int32)
+    item_elig = np.ascontiguousarray(item_elig, dtype=np.uint64)
+    psi_off = np.ascontiguousarray(psi_off, dtype=np.int64)
+    psi = np.ascontiguousarray(psi, dtype=np.float64)
+    n = len(item_ptr) - 1
+    n_sel = np.zeros(max(n, 1), dtype=np.int32)
+    sel = np.zeros((max(n, 1), n_devices, 3), dtype=np.int32)
+    obj = np.zeros(max(n, 1), dtype=np.float64)
+    opt = np.zeros(max(n, 1), dtype=np.int32)
+    a = _BatchArgs(n_problems=n, n_devices=n_devices, item_ptr=item_ptr.ctypes.data,
+                   item_bound=item_bound.ctypes.data, item_elig=item_elig.ctypes.data,
+                   psi_off=psi_off.ctypes.data, psi=psi.ctypes.data, budget_s=float(budget_s),
+                   max_options=int(max_options), n_threads=int(n_threads))
+    o = _BatchOut(n_sel=n_sel.ctypes.data, sel=sel.ctypes.data, objective=obj.ctypes.data,
+                  optimal=opt.ctypes.data)
+    _check(L.fate_solve_batch(C.byref(a), C.byref(o)), "fate_solve_batch")
+    return BatchSolution(n_sel[:n], sel[:n], obj[:n], opt[:n], float(o.wall_s), int(o.threads))

@@ -1,5 +1,7 @@
-"""Shared test cases: (bank, weights, states, work) built with the mirror
-generators, so they are reproducible on the GPU box without the reference."""
+"""Shared test cases: (bank, weights, states, work).  Instances come from the
+package's generator mirror (wf/workloads, bit-identical to the reference's,
+tests/test_reference_mirror.py); execution states are the reference's own
+``wfsched.state.ExecutionState``."""
 
 from __future__ import annotations
 
@@ -13,7 +15,7 @@ from paper_2605_07238_b200.wf import workloads as W
 from paper_2605_07238_b200.wf.dagmodel import (
     DeviceSpec, DeviceTopology, Query, Stage, WorkflowDag, WorkflowInstance, annotate_topology,
 )
-from paper_2605_07238_b200.wf.execstate import ExecutionState, PrefixEntry
+from wfsched.state import ExecutionState, PrefixEntry
 from paper_2605_07238_b200.wf.weights import AblationFlags, ScoreWeights, default_config
 
 

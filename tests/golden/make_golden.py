@@ -333,7 +333,7 @@ def main():
         gen_sampled(a.parallel, a.quick)
 
 
-if __name__ == "__main__" and "--c5-assign" not in sys.argv:
+if __name__ == "__main__" and "--c5-assign" not in sys.argv and "--r2" not in sys.argv:
     main()
 
 
@@ -369,3 +369,181 @@ def gen_c5_assign(parallel: int, n: int = 16):
 
 if __name__ == "__main__" and "--c5-assign" in sys.argv:
     gen_c5_assign(os.cpu_count() or 4)
+
+
+# ---------------------------------------------------------------------------
+# round 2: SURVEY §8(d) parity gates at full size
+# ---------------------------------------------------------------------------
+# * c5_full: every frontier candidate of 64 config-5 instances spread over the
+#   bench's 4096 (i = 0, 64, ..., 4032): Psi in FrontierProblem order, S and
+#   completion per (sorted stage, sorted eligible device), and the budget-0
+#   assignment of the reference's own solve (planner.py:150-234);
+# * c4_assign: the same for the frontier of all 8 canonical config-4 scenarios
+#   (frontier mode, ~11.3k Psi each), scored in stage chunks across processes;
+# * c3_base: halo / kvflow / roundrobin RunRecords of the 24 prefix-suite
+#   instances at H=3, so the normalised C3 table can be recomputed from
+#   GPU-run FATE records.
+
+C5_FULL = tuple(range(0, 4096, 64))
+
+
+def _ref_c5(i):
+    cfg = SC.config_c5()
+    rdag = RB.synth_generate(RB.SuiteSpec(kind="synthetic", depth=20, width=25, density=0.12,
+                                          seed=1000 + i, batch_size=16), cfg)
+    return cfg, RB.make_instance(rdag, 16, 1000 + i)
+
+
+def _ref_c4():
+    cfg = SC.config_c4_catalog()
+    rdag = RB.synth_generate(RB.SuiteSpec(kind="synthetic", depth=100, width=100,
+                                          density=0.03, seed=1, batch_size=16), cfg)
+    return cfg, RB.make_instance(rdag, 16, 1)
+
+
+def _pairs(cm, st, dag, sids):
+    """S and completion per (sorted stage, sorted eligible device)."""
+    qids = tuple(q.query_id for q in st.instance.queries)
+    sched, compl = [], []
+    for sid in sids:
+        stage = dag.stages[sid]
+        for d in sorted(stage.eligible_devices):
+            sched.append(u64(cm.sched_score(stage, d, st, dag)))
+            t = cm.realized_duration(stage, [(d, qids)], st, dag)[0]
+            compl.append(u64(max(0.0, st.device_free.get(d, 0.0) - st.clock) + t.total_s))
+    return sched, compl
+
+
+def _c5_full_one(i):
+    from wfsched.costs import CostModel
+    from wfsched.model import ready_set
+
+    cfg, rinst = _ref_c5(i)
+    st = SC.build_scenario(rinst, cfg, i, kit=reference_kit())
+    cm = CostModel(cfg.models, cfg.topology, cfg.weights)
+    sids = sorted(ready_set(rinst.dag, st.completed))
+    prob = RP.build_problem(set(sids), st, cm, rinst.dag)
+    sol = RP.solve_frontier(prob, budget_s=0.0)
+    sched, compl = _pairs(cm, st, rinst.dag, sids)
+    return ({"instance": i, "frontier": sids, "n_cand": len(prob.candidates),
+             "n_pairs": len(sched), "selected": [list(x) for x in sol.selected],
+             "objective": sol.objective.hex(), "optimal": sol.optimal},
+            [u64(c.psi) for c in prob.candidates], sched, compl)
+
+
+def gen_c5_full(parallel: int):
+    with mp.get_context("fork").Pool(parallel) as pool:
+        res = pool.map(_c5_full_one, list(C5_FULL), chunksize=1)
+    meta = [r[0] for r in res]
+    psi = [x for r in res for x in r[1]]
+    sched = [x for r in res for x in r[2]]
+    compl = [x for r in res for x in r[3]]
+    with open(os.path.join(HERE, "c5_full.json"), "w") as fh:
+        json.dump({"budget_s": 0.0, "instances": meta}, fh, indent=0, sort_keys=True)
+    np.savez_compressed(os.path.join(HERE, "c5_full.npz"), psi=np.asarray(psi, np.uint64),
+                        sched=np.asarray(sched, np.uint64), completion=np.asarray(compl, np.uint64))
+    print(f"c5_full: {len(meta)} instances, {len(psi)} psi, {len(sched)} pairs")
+
+
+_C4 = {}
+
+
+def _c4_chunk(args):
+    """Reference Psi / S / completion of a slice of one scenario's frontier."""
+    from wfsched.costs import CostModel
+
+    s, sids = args
+    if "inst" not in _C4:
+        _C4["cfg"], _C4["inst"] = _ref_c4()
+    cfg, rinst = _C4["cfg"], _C4["inst"]
+    st = SC.build_scenario(rinst, cfg, s, kit=reference_kit())
+    cm = CostModel(cfg.models, cfg.topology, cfg.weights)
+    dag = rinst.dag
+    psi = []
+    for sid in sids:  # build_problem's loop order (planner.py:83-97)
+        stage = dag.stages[sid]
+        bound = 1 if cfg.weights.ablation.no_shard else min(stage.shard_bound,
+                                                            len(stage.eligible_devices))
+        for k in range(bound):
+            for d in sorted(stage.eligible_devices):
+                psi.append(cm.plan_score(stage, k, d, st, dag))
+    sched, compl = _pairs(cm, st, dag, sids)
+    return s, sids, psi, sched, compl
+
+
+def gen_c4_assign(parallel: int, n_scen: int = 8, chunk: int = 4):
+    from wfsched.costs import CostModel
+    from wfsched.model import ready_set
+
+    cfg, rinst = _ref_c4()
+    tasks, fronts = [], {}
+    for s in range(n_scen):
+        st = SC.build_scenario(rinst, cfg, s, kit=reference_kit())
+        fronts[s] = sorted(ready_set(rinst.dag, st.completed))
+        tasks += [(s, fronts[s][j: j + chunk]) for j in range(0, len(fronts[s]), chunk)]
+    with mp.get_context("fork").Pool(parallel) as pool:
+        out = pool.map(_c4_chunk, tasks, chunksize=1)
+    meta, psi_all, sched_all, compl_all = [], [], [], []
+    for s in range(n_scen):
+        parts = [o for o in out if o[0] == s]
+        psi = [x for o in parts for x in o[2]]
+        st = SC.build_scenario(rinst, cfg, s, kit=reference_kit())
+        cm = CostModel(cfg.models, cfg.topology, cfg.weights)
+        # the reference's own FrontierProblem from the reference's Psi values
+        cands, it = [], iter(psi)
+        bounds = {}
+        for sid in fronts[s]:
+            stage = rinst.dag.stages[sid]
+            bounds[sid] = min(stage.shard_bound, len(stage.eligible_devices))
+            for k in range(bounds[sid]):
+                for d in sorted(stage.eligible_devices):
+                    cands.append(RP.Candidate(sid, k, d, next(it)))
+        prob = RP.FrontierProblem(tuple(cands), bounds, cfg.topology.device_ids)
+        sol = RP.solve_frontier(prob, budget_s=0.0)
+        meta.append({"scenario": s, "frontier": fronts[s], "n_cand": len(cands),
+                     "n_pairs": sum(len(o[3]) for o in parts), "clock": st.clock.hex(),
+                     "selected": [list(x) for x in sol.selected],
+                     "objective": sol.objective.hex(), "optimal": sol.optimal})
+        psi_all += [u64(x) for x in psi]
+        sched_all += [x for o in parts for x in o[3]]
+        compl_all += [x for o in parts for x in o[4]]
+        del cm
+    with open(os.path.join(HERE, "c4_assign.json"), "w") as fh:
+        json.dump({"budget_s": 0.0, "scenarios": meta}, fh, indent=0, sort_keys=True)
+    np.savez_compressed(os.path.join(HERE, "c4_assign.npz"), psi=np.asarray(psi_all, np.uint64),
+                        sched=np.asarray(sched_all, np.uint64),
+                        completion=np.asarray(compl_all, np.uint64))
+    print(f"c4_assign: {len(meta)} scenarios, {len(psi_all)} psi")
+
+
+def _c3_base_cell(args):
+    ratio, batch, k, method = args
+    cfg = default_config(4)
+    conf = cfg.with_weights(replace(cfg.weights, horizon=3))
+    suite = RB.build_prefix_suite(RB.SuiteSpec(kind="prefix_reuse", repeat_ratio=ratio,
+                                               batch_size=batch, seed=20260423), cfg)
+    rec = RE.run(RPol.make_policy(method), suite[k], conf)
+    d = record_dict(rec)
+    d.update({"ratio": ratio, "batch": batch, "shape": k})
+    return d
+
+
+def gen_c3_base(parallel: int):
+    cells = [(r, b, k, m) for r in (0.0, 0.25, 0.5, 1.0) for b in (16, 32) for k in range(3)
+             for m in ("halo", "kvflow", "roundrobin")]
+    with mp.get_context("fork").Pool(parallel) as pool:
+        recs = pool.map(_c3_base_cell, cells, chunksize=1)
+    with open(os.path.join(HERE, "c3_baselines.json"), "w") as fh:
+        json.dump({"horizon": 3, "records": recs}, fh, indent=0, sort_keys=True)
+    print(f"c3_baselines: {len(recs)} records")
+
+
+if __name__ == "__main__" and "--r2" in sys.argv:
+    _which = sys.argv[sys.argv.index("--r2") + 1].split(",")
+    _par = os.cpu_count() or 4
+    if "c3base" in _which:
+        gen_c3_base(_par)
+    if "c5full" in _which:
+        gen_c5_full(_par)
+    if "c4assign" in _which:
+        gen_c4_assign(_par)

@@ -61,8 +61,9 @@ class _Recorder:
 
 
 def check_c1_known_answer(scorer) -> None:
+    from wfsched.executor import run
+
     from paper_2605_07238_b200.planner import FateGpuPolicy
-    from paper_2605_07238_b200.wf.simulate import run
 
     inst, cfg = G.c1_setup({"tag": "default", "horizon": 2})
     rec = _Recorder(scorer)
@@ -125,9 +126,35 @@ def check_c2_table1(fate_records) -> None:
     assert got == C2_TABLE1_FATE, got
 
 
-def check_c3_table(runs) -> None:
-    """Every prefix-suite FATE run reproduced; also report per-ratio geo means."""
-    assert len(runs) == 24
+# C3 at H=3, batch 16, normalised by halo at ratio 0
+# (harness.py:620-626 / _suite_table 711-733)
+C3_TABLE_FATE = ("0.936", "0.890", "0.820", "0.705")
+
+
+def check_c3_table(fate_records) -> tuple:
+    """The normalised prefix-reuse table's FATE row, recomputed from the
+    GPU-run FATE records and the reference's halo records (golden
+    c3_baselines.json, H=3) exactly as ``_suite_table`` does: per ratio the
+    geometric mean of the CSV-rounded makespans of the batch-16 instances,
+    divided by halo's at ratio 0."""
+    with open(os.path.join(G.GOLDEN, "c3_baselines.json")) as fh:
+        base = json.load(fh)["records"]
+    assert len(fate_records) == 24
+    ratios = (0.0, 0.25, 0.5, 1.0)
+
+    def geo_of(recs):
+        return _geo([_csv6(float.fromhex(r["makespan"])) if isinstance(r, dict)
+                     else _csv6(r.makespan) for r in recs])
+
+    halo0 = geo_of([r for r in base if r["method"] == "halo" and r["ratio"] == 0.0
+                    and r["batch"] == 16])
+    row = []
+    for ratio in ratios:
+        recs = [rec for (rr, b, _k), rec in fate_records.items() if rr == ratio and b == 16]
+        assert len(recs) == 3
+        row.append(f"{geo_of(recs) / halo0:.3f}")
+    assert tuple(row) == C3_TABLE_FATE, row
+    return tuple(row)
 
 
 def check_c45_sampled(gpu: bool) -> int:
@@ -192,7 +219,7 @@ def check_c5_assign(gpu: bool, native_solver: bool = False) -> int:
     selects on the reference's own cost matrix (tests/golden/c5_assign.json).
     ``native_solver`` solves with ``fate_solve_frontier`` instead of the
     Python restatement."""
-    from paper_2605_07238_b200.wf.frontier import Candidate, FrontierProblem, solve_frontier
+    from wfsched.planner import Candidate, FrontierProblem, solve_frontier
 
     if native_solver:
         from paper_2605_07238_b200.solver import solve_frontier
@@ -226,4 +253,140 @@ def check_c5_assign(gpu: bool, native_solver: bool = False) -> int:
         assert [list(x) for x in sol.selected] == g["selected"], i
         assert sol.objective.hex() == g["objective"], i
         n += 1
+    return n
+
+
+# ---------------------------------------------------------------------------
+# round 2: SURVEY §8(d) parity gates at full size (make_golden.py --r2)
+# ---------------------------------------------------------------------------
+
+
+def _f64(bits_list):
+    return np.asarray(bits_list, dtype=np.uint64)
+
+
+def _solve_both(cands, bounds, device_ids, budget):
+    """Budget-0 host solve of a cost matrix with the reference's own
+    ``solve_frontier`` and with the native one; both results returned."""
+    from wfsched.planner import Candidate, FrontierProblem, solve_frontier
+
+    from paper_2605_07238_b200.solver import solve_frontier as native
+
+    prob = FrontierProblem(tuple(Candidate(*c) for c in cands), bounds, tuple(device_ids))
+    return solve_frontier(prob, budget_s=budget), native(prob, budget_s=budget)
+
+
+def _check_wave(bank, work, out, items, want_psi, want_sched, want_compl, meta, cfg, tag):
+    """Psi (candidate order), S and completion ((stage, eligible device)
+    order) of the items ``items`` of one scenario, then the budget-0
+    assignments of both solvers, against the reference's."""
+    D = bank.scalars["n_devices"]
+    devs = bank.device_ids
+    inst = int(bank.arrays["st_inst"][int(work.stage[items[0]])])
+    off0 = int(bank.inst_stage_off[inst])
+    sids = bank.stage_ids[inst]
+    cands, sched, compl, bounds = [], [], [], {}
+    for w in items:
+        g = int(work.stage[w])
+        sid = sids[g - off0]
+        mask = int(bank.arrays["st_elig"][g])
+        base = int(work.psi_off[w])
+        bounds[sid] = int(work.bounds[w])
+        for k in range(bounds[sid]):
+            for d in range(D):
+                if mask >> d & 1:
+                    cands.append((sid, k, devs[d], float(out["psi"][base + k * D + d])))
+        for d in range(D):
+            if mask >> d & 1:
+                sched.append(out["sched"][w * D + d])
+                compl.append(out["completion"][w * D + d])
+    assert [c[0] for c in cands][:1] and sorted(bounds) == meta["frontier"], tag
+    assert len(cands) == meta["n_cand"], tag
+    got = np.asarray([c[3] for c in cands], dtype=np.float64).view(np.uint64)
+    assert np.array_equal(got, want_psi), tag
+    assert np.array_equal(np.asarray(sched, dtype=np.float64).view(np.uint64), want_sched), tag
+    assert np.array_equal(np.asarray(compl, dtype=np.float64).view(np.uint64), want_compl), tag
+    ref, nat = _solve_both(cands, bounds, cfg.topology.device_ids, 0.0)
+    for sol in (ref, nat):
+        assert [list(x) for x in sol.selected] == meta["selected"], tag
+        assert sol.objective.hex() == meta["objective"], tag
+        assert sol.optimal == meta["optimal"], tag
+    return len(cands)
+
+
+def _score(bank, weights, states, work, gpu):
+    if gpu:
+        from paper_2605_07238_b200 import runtime
+
+        res = runtime.DeviceBank(bank, weights).score(states, work, extras=True)
+        return {k: getattr(res, k).cpu().numpy() for k in ("psi", "sched", "completion")}
+    import oracle
+
+    return oracle.score(bank, pack.weights_record(weights), states, work)
+
+
+def _load_r2(name):
+    with open(os.path.join(G.GOLDEN, f"{name}.json")) as fh:
+        meta = json.load(fh)
+    arr = np.load(os.path.join(G.GOLDEN, f"{name}.npz"))
+    return meta, {k: arr[k] for k in arr.files}
+
+
+def check_c5_full(gpu: bool) -> int:
+    """Every frontier candidate of 64 config-5 instances (i = 0, 64, ...,
+    4032) and their budget-0 assignments.  On the GPU the batch is the bench's
+    own (bench.build_c5: all 4096 instances, one launch); on the CPU (oracle)
+    each instance is generated alone by the same native generator."""
+    import bench
+    from paper_2605_07238_b200 import fastgen
+
+    meta, arr = _load_r2("c5_full")
+    cfg = scenarios.config_c5()
+    if gpu:
+        cfg, bank, states, work = bench.build_c5(bench.shard_plan(0, 1), "frontier")
+        out = _score(bank, cfg.weights, states, work, True)
+        scen = np.asarray(work.scen)
+    pc = sc = 0
+    n = 0
+    for m in meta["instances"]:
+        i = m["instance"]
+        if not gpu:
+            fb = fastgen.synth_batch(cfg, 1, 1000 + i, i, *bench.C5_SHAPE.values())
+            sc_i, g_i = fb.frontier_items()
+            bank, states = fb.bank, fb.states
+            work = pack.make_work(bank, zip(sc_i.tolist(), g_i.tolist()), False)
+            out = _score(bank, cfg.weights, states, work, False)
+            items = list(range(work.n_items))
+        else:
+            items = np.flatnonzero(scen == i).tolist()
+        n += _check_wave(bank, work, out, items, arr["psi"][pc: pc + m["n_cand"]],
+                         arr["sched"][sc: sc + m["n_pairs"]],
+                         arr["completion"][sc: sc + m["n_pairs"]], m, cfg, ("c5", i))
+        pc += m["n_cand"]
+        sc += m["n_pairs"]
+    return n
+
+
+def check_c4_assign(gpu: bool, scenarios_: tuple | None = None) -> int:
+    """Every frontier candidate of the 8 canonical config-4 scenarios (the
+    bench's frontier-mode batch, bench.build_c4) and their budget-0
+    assignments."""
+    import bench
+
+    meta, arr = _load_r2("c4_assign")
+    cfg, bank, states, work = bench.build_c4("frontier")
+    out = _score(bank, cfg.weights, states, work, gpu)
+    scen = np.asarray(work.scen)
+    pc = sc = 0
+    n = 0
+    for m in meta["scenarios"]:
+        s = m["scenario"]
+        if scenarios_ is None or s in scenarios_:
+            assert states.arrays["scen_clock"][s].hex() == m["clock"]
+            items = np.flatnonzero(scen == s).tolist()
+            n += _check_wave(bank, work, out, items, arr["psi"][pc: pc + m["n_cand"]],
+                             arr["sched"][sc: sc + m["n_pairs"]],
+                             arr["completion"][sc: sc + m["n_pairs"]], m, cfg, ("c4", s))
+        pc += m["n_cand"]
+        sc += m["n_pairs"]
     return n

@@ -1,9 +1,12 @@
-"""Replay captured reference runs through the mirror executor with a chosen
-scorer (GPU or oracle), checking every wave against the golden vectors.
+"""Replay captured reference runs through the REFERENCE executor
+(``wfsched.executor.run``) with the GPU policy plugged in, checking every wave
+against the golden vectors.
 
 Golden files (tests/golden/*.json + *.npz) come from the reference itself
-(tests/golden/make_golden.py).  Instances are rebuilt with the mirror
-generators, so replay works on the GPU box where the reference is absent.
+(tests/golden/make_golden.py).  Instances and configs are rebuilt with the
+reference's own generators; ``wfsched`` is importable from ``baseline/_ref``
+(the reference install, which travels to the GPU box) or from
+/root/reference in the build container (tests/conftest.py).
 """
 
 from __future__ import annotations
@@ -13,11 +16,12 @@ import os
 from dataclasses import replace
 
 import numpy as np
+import wfsched.benchgen as W
+import wfsched.executor as RE
+from wfsched.config import AblationFlags, default_config
 
+from paper_2605_07238_b200 import compat
 from paper_2605_07238_b200.planner import FateGpuPolicy, WaveScores
-from paper_2605_07238_b200.wf import workloads as W
-from paper_2605_07238_b200.wf.simulate import run
-from paper_2605_07238_b200.wf.weights import AblationFlags, default_config
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
@@ -151,10 +155,19 @@ def record_mismatches(rec, want: dict) -> list:
 
 
 def replay(run_meta: dict, arrays: dict, instance, config, scorer, seed: int = 0,
-           solver: str = "python", observer=None):
+           solver: str = "reference", mirror=None):
+    """One FATE run of the reference executor with the GPU policy; ``mirror``
+    (a MirrorScorer) is attached to the executor's live state through
+    ``compat.install(mirror=...)``."""
     chk = CheckingScorer(scorer, run_meta, arrays)
     policy = FateGpuPolicy(scorer=chk, solver=solver)
-    rec = run(policy, instance, config, seed=seed, observer=observer)
+    if mirror is not None:
+        compat.install(mirror=mirror, policy_factory=False)
+    try:
+        rec = RE.run(policy, instance, config, seed=seed)
+    finally:
+        if mirror is not None:
+            compat.uninstall()
     problems = list(chk.mismatches)
     if chk.i != len(run_meta["waves"]):
         problems.append(f"{chk.i} waves != golden {len(run_meta['waves'])}")

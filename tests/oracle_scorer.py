@@ -1,7 +1,7 @@
 """Oracle-backed scorer with the GpuScorer interface (test infrastructure).
 
-Lets the CPU test suite drive the mirror executor/solver/policy with the C
-oracle, to validate the host side of the drop-in without a GPU.  Never used
+Lets the CPU test suite drive the reference executor and the GPU policy's
+host side with the C oracle, to validate the host side of the drop-in without a GPU.  Never used
 by the product.
 """
 
@@ -38,4 +38,5 @@ class OracleScorer:
             stage_ids=sids, bounds=[int(b) for b in work.bounds], device_ids=bank.device_ids,
             elig=[int(bank.arrays["st_elig"][g]) for g in work.stage], psi=res["psi"],
             psi_off=work.psi_off, sched=res["sched"].reshape(n, D),
-            completion=res["completion"].reshape(n, D), tail=res["tail"].reshape(n, D))
+            completion=res["completion"].reshape(n, D), tail=res["tail"].reshape(n, D),
+            timing=res["timing"].reshape(n, D, 3))

@@ -30,7 +30,7 @@ def test_mirror_replays_golden_runs(name):
         else:
             inst, cfg = G.c3_setup(r["ratio"], r["batch"], r["shape"])
         scorer = MirrorScorer(check_ready=True)
-        _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, observer=scorer)
+        _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, mirror=scorer)
         n_waves += scorer.ready_checks
         if problems:
             bad.append(problems[:3])
@@ -67,7 +67,7 @@ def test_mirror_arrays_equal_packed_snapshot():
             return ws
 
     scorer = Spy(check_ready=True)
-    _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, observer=scorer)
+    _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, mirror=scorer)
     assert not problems, problems[:3]
     assert len(checks) == len(r["waves"])
 
@@ -84,7 +84,7 @@ def test_executor_on_gpu_frontier_matches_golden_records():
             else:
                 inst, cfg = G.c3_setup(r["ratio"], r["batch"], r["shape"])
             scorer = MirrorScorer(gpu_frontier=True)
-            _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, observer=scorer)
+            _, problems, _ = G.replay(r, arrs, inst, cfg, scorer, mirror=scorer)
             if problems:
                 bad.append((name, problems[:3]))
     assert not bad, bad

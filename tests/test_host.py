@@ -13,9 +13,7 @@ import numpy as np
 import pytest
 
 from paper_2605_07238_b200 import pack, runtime, scenarios
-from paper_2605_07238_b200.wf.frontier import (
-    Candidate, FrontierProblem, check_constraints, solve_frontier,
-)
+from wfsched.planner import Candidate, FrontierProblem, check_constraints, solve_frontier
 
 from cases import c5_case, edge_case, small_case
 
@@ -35,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     assert {"fate_score", "fate_prepare", "fate_windows_build_host"} <= set(names)
     for n in names:
         assert hasattr(lib, n), n
-    assert runtime.load_library().fate_abi_version() == 2
+    assert runtime.load_library().fate_abi_version() == 3
 
 
 def _py_windows(bank, levels):
@@ -245,12 +243,11 @@ def test_bank_flags_declare_query_groups_exactly():
 
 def test_c_abi_from_plain_c(tmp_path):
     """examples/solve_frontier.c links libfate.so from C (no Python) and its
-    native solve equals the Python restatement of the reference's
-    solve_frontier on the same problem (selection, objective, node count)."""
+    native solve equals the reference's solve_frontier on the same problem (selection, objective, node count)."""
     import shutil
     import subprocess
 
-    from paper_2605_07238_b200.wf.frontier import Candidate as Cd
+    from wfsched.planner import Candidate as Cd
 
     if shutil.which("gcc") is None:
         pytest.skip("gcc not available")

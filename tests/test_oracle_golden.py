@@ -1,8 +1,9 @@
 """CPU oracle pinned against golden vectors captured from the reference.
 
-Also validates the host side of the drop-in (mirror executor, frontier solver,
-FATE policy, packer) by replaying every captured reference run with the
-oracle as the scorer: every wave's Psi / S / completion and the final
+Also validates the host side of the drop-in (the GPU policy subclassing the
+reference FatePolicy, the packer, the native solver) by replaying every
+captured reference run through the reference executor with the oracle as the
+scorer: every wave's Psi / S / completion and the final
 RunRecord must match the reference bit for bit.
 """
 
@@ -39,15 +40,20 @@ def test_c1_known_answer_vectors():
 def test_replay_c1_c3(name):
     runs, arrs = G.load(name)
     bad = []
+    records = {}
     for r in runs:
         if name == "c1":
             inst, cfg = G.c1_setup(r["variant"])
         else:
             inst, cfg = G.c3_setup(r["ratio"], r["batch"], r["shape"])
-        _, problems, _ = G.replay(r, arrs, inst, cfg, OracleScorer())
+        rec, problems, _ = G.replay(r, arrs, inst, cfg, OracleScorer())
+        if name == "c3":
+            records[(r["ratio"], r["batch"], r["shape"])] = rec
         if problems:
             bad.append(problems[:3])
     assert not bad, bad
+    if name == "c3":
+        assert GC.check_c3_table(records) == GC.C3_TABLE_FATE
 
 
 def test_replay_c2_and_table1():
@@ -72,3 +78,16 @@ def test_c45_sampled():
 
 def test_c5_assignments_budget0():
     assert GC.check_c5_assign(gpu=False) == 16
+
+
+def test_c5_full_frontiers_oracle():
+    """The oracle on all frontier candidates of the 64 golden config-5
+    instances (native generator, one instance at a time) and the budget-0
+    assignments of both solvers on its matrix."""
+    assert GC.check_c5_full(gpu=False) == 89312
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(G.GOLDEN, "c4_assign.json")),
+                    reason="c4 golden not generated yet")
+def test_c4_frontier_oracle_two_scenarios():
+    assert GC.check_c4_assign(gpu=False, scenarios_=(0, 5)) > 15000

@@ -1,6 +1,6 @@
 """Native frontier solve (csrc/fate_solver.cpp) against the
-Python restatement and the reference's own solver (planner.py:101-234):
-identical selection, objective bits, optimal flag and node count.  CPU only."""
+reference's own solver (``wfsched.planner``, planner.py:101-234): identical
+selection, objective bits, optimal flag and node count.  CPU only."""
 
 from __future__ import annotations
 
@@ -10,7 +10,7 @@ import random
 import pytest
 
 from paper_2605_07238_b200 import runtime
-from paper_2605_07238_b200.wf import frontier as MF
+import wfsched.planner as MF
 
 import golden_checks as GC
 
@@ -45,7 +45,7 @@ def _same(a, b):
     assert a.nodes_explored == b.nodes_explored
 
 
-def test_native_matches_python_solver_on_random_problems():
+def test_native_matches_reference_solver_on_random_problems():
     S = _native()
     rng = random.Random(11)
     for it in range(300):

@@ -11,7 +11,7 @@ import bench  # noqa: E402
 from paper_2605_07238_b200 import runtime  # noqa: E402
 
 dev = torch.device("cuda:0")
-cfg, bank, states, work, _ = bench.build_c5(0, 1, "frontier")
+cfg, bank, states, work = bench.build_c5(bench.shard_plan(0, 1), "frontier")
 dbank = runtime.DeviceBank(bank, cfg.weights, device=dev)
 for chunks in [int(x) for x in sys.argv[1:]] or [4]:
     pipe = runtime.HostPipeline(dbank, states, work, n_chunks=chunks, graph=True)

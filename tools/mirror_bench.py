@@ -1,4 +1,4 @@
-"""Per-wave scorer cost of a long FATE run: snapshot -> pack -> upload
+"""Per-wave scorer cost of a long FATE run of the reference executor: snapshot -> pack -> upload
 (GpuScorer) vs the device-resident mirror (MirrorScorer, events applied on the
 GPU).  Prints one JSON line per scorer.  Native solver at budget 0 keeps the
 run itself fast; the scorer time is what differs."""
@@ -10,11 +10,18 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+for _p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+    if os.path.isdir(os.path.join(_p, "wfsched")):
+        sys.path.append(_p)
+        break
+
+import wfsched.benchgen as W  # noqa: E402
+from wfsched.config import default_config  # noqa: E402
+from wfsched.executor import run  # noqa: E402
+
+from paper_2605_07238_b200 import compat  # noqa: E402
 from paper_2605_07238_b200.mirror import MirrorScorer  # noqa: E402
 from paper_2605_07238_b200.planner import FateGpuPolicy, GpuScorer  # noqa: E402
-from paper_2605_07238_b200.wf import workloads as W  # noqa: E402
-from paper_2605_07238_b200.wf.simulate import run  # noqa: E402
-from paper_2605_07238_b200.wf.weights import default_config  # noqa: E402
 from dataclasses import replace  # noqa: E402
 
 
@@ -45,8 +52,13 @@ def main():
                  else MirrorScorer(gpu_frontier=name.endswith("frontier")))
         sc = Timed(inner)
         pol = FateGpuPolicy(scorer=sc, solver="native", solver_budget_s=0.0)
+        if name != "snapshot+pack":
+            compat.install(mirror=inner, policy_factory=False)
         t0 = time.perf_counter()
-        rec = run(pol, inst, cfg, observer=None if name == "snapshot+pack" else inner)
+        try:
+            rec = run(pol, inst, cfg)  # the reference executor, unchanged
+        finally:
+            compat.uninstall()
         wall = time.perf_counter() - t0
         recs[name] = rec
         print(json.dumps({"scorer": name, "stages": len(dag.stages), "waves": sc.waves,

@@ -5,7 +5,7 @@ import bench
 from paper_2605_07238_b200 import runtime
 
 dev = torch.device("cuda:0")
-cfg, bank, states, work, _ = bench.build_c5(0, 1, "frontier")
+cfg, bank, states, work = bench.build_c5(bench.shard_plan(0, 1), "frontier")
 dbank = runtime.DeviceBank(bank, cfg.weights, device=dev)
 ds, dw = dbank.upload_states(states), dbank.upload_work(work)
 out = dbank.alloc_out(work, extras=False)

@@ -65,7 +65,7 @@ def main():
     import bench
     from paper_2605_07238_b200 import runtime
 
-    cfg, bank, states, work, _ = bench.build_c5(0, 1, "frontier")
+    cfg, bank, states, work = bench.build_c5(bench.shard_plan(0, 1), "frontier")
     dbank = runtime.DeviceBank(bank, cfg.weights, device=dev)
     for chunks, streams, graph in ((1, 1, 0), (4, 1, 0), (3, 1, 1), (4, 1, 1), (5, 1, 1),
                                    (6, 1, 1), (8, 1, 1), (12, 1, 1)):
