@@ -63,6 +63,16 @@ HBM_FALLBACK_GBS = 6650.0
 # ---------------------------------------------------------------------------
 
 
+def reference_on_path() -> None:
+    """The reference package (``wfsched``), installed unmodified in
+    baseline/_ref (travels to the GPU box) or the build container's tree."""
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "wfsched")):
+            if p not in sys.path:
+                sys.path.append(p)
+            return
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -461,6 +471,7 @@ def reference_solve_check(bank, work, psi_host, sol, n_check: int = 8) -> dict |
     reference package; outside every timed region)."""
     import numpy as np
 
+    reference_on_path()
     try:
         import wfsched.planner as RP
     except ImportError:
@@ -548,9 +559,7 @@ def _reference_pool(n_pool: int):
     """Config-5 instances and their canonical scenario states built with the
     reference's OWN generators and state type (wfsched, installed unmodified
     in baseline/_ref), packed by the pure-Python packer: no libfate.so."""
-    ref = os.path.join(ROOT, "baseline", "_ref")
-    if os.path.isdir(os.path.join(ref, "wfsched")) and ref not in sys.path:
-        sys.path.append(ref)
+    reference_on_path()
     import wfsched.benchgen as RB
 
     from paper_2605_07238_b200 import pack, scenarios

@@ -64,11 +64,19 @@ def ptx_contraction_free(text: str) -> bool:
     return re.search(r"\bfma\.rn\.f64\b", rest) is None
 
 
+def ab_build() -> bool:
+    """FATE_BUILD_AB=1: experiment build with the previous kernel generation
+    and the environment A/B knobs compiled in (-DFATE_AB).  Production builds
+    run exactly one kernel generation with the measured launch shape."""
+    return os.environ.get("FATE_BUILD_AB", "") not in ("", "0")
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-shared", "-Xptxas", "-v", *SOURCES, "-o", tmp]
+    extra = ["-DFATE_AB"] if ab_build() else []
+    cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-shared", "-Xptxas", "-v", *SOURCES, "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -16,7 +16,7 @@
 //
 // Work decomposition: one "item" = (scenario, stage v) is scored by one warp
 // (fate_score_v6.cuh, the production kernel; fate_score_v5.cuh is the previous
-// generation, kept for A/B).  This file holds the shared device helpers, the
+// generation, compiled only into -DFATE_AB experiment builds).  This file holds the shared device helpers, the
 // prologue kernels of fate_prepare (mean_base, demand, split penalty, edge
 // terms, static tail tables, stage records, op templates), the wire-format
 // unpack kernel of the host pipeline, and the C ABI.
@@ -31,6 +31,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "fate.h"
 #include "fate_internal.h"
@@ -226,8 +228,22 @@ __global__ void fate_prepare_demand_kernel(fate_bank b, fate_windows win, fate_d
 }
 
 #include "fate_prologue.cuh"
+#ifdef FATE_AB
 #include "fate_score_v5.cuh"
+#endif
 #include "fate_score_v6.cuh"
+
+// A/B knobs.  The production library (built without FATE_AB) runs exactly
+// one kernel generation with the measured launch shape; a build with
+// -DFATE_AB (FATE_BUILD_AB=1 python -m paper_2605_07238_b200.build) adds the
+// previous generation v5 and reads the environment overrides below, for
+// experiments only.
+#ifdef FATE_AB
+int ab_env(const char* name, int dflt, int lo, int hi) {
+    const char* e = getenv(name);
+    return e ? std::max(lo, std::min(hi, atoi(e))) : dflt;
+}
+#endif
 
 template <int DPL, bool OVR, bool SL, int MINB, bool QG>
 int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
@@ -235,12 +251,12 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
                  const fate_out* out, cudaStream_t s) {
     if (!der->stage_rec || (win->levels > 0 && (!der->tmpl_ptr || !der->tmpl)))
         return fail(FATE_ENOTREADY, "v6 kernel needs stage records and op templates");
-    static int opcap_env = -1;
-    if (opcap_env < 0) {
-        const char* e = getenv("FATE_V6_OPCAP");
-        opcap_env = e ? std::max(32, std::min(4096, atoi(e))) & ~3 : 0;
-    }
+#ifdef FATE_AB
+    static const int opcap_env = ab_env("FATE_V6_OPCAP", 0, 32, 4096) & ~3;
     const int opcap = opcap_env > 0 ? opcap_env : v6_opcap_default<DPL>();
+#else
+    const int opcap = v6_opcap_default<DPL>();
+#endif
     constexpr bool maskw = !OVR && DPL == 2;
     const V6Layout lay =
         SL ? v6_layout_static<DPL>(win->max_level_ops, bank->n_models, maskw, opcap)
@@ -269,14 +285,14 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
         occ_fn = fn;
     }
     // items per ticket: 2 for one device slot per lane, 1 for two (heavier
-    // items: finer tail balance beats fewer atomics); 0 = guided sizes.
-    // Measured on B200 at the current register budgets.
-    static int fetch_env = -2;
-    if (fetch_env == -2) {
-        const char* e = getenv("FATE_V6_FETCH");
-        fetch_env = e ? std::max(0, std::min(64, atoi(e))) : -1;
-    }
+    // items: finer tail balance beats fewer atomics).  Measured on B200 at
+    // the current register budgets (A/B: 0 = guided sizes).
+#ifdef FATE_AB
+    static const int fetch_env = ab_env("FATE_V6_FETCH", -1, 0, 64);
     const int fetch = fetch_env >= 0 ? fetch_env : (DPL == 1 ? 2 : 1);
+#else
+    const int fetch = DPL == 1 ? 2 : 1;
+#endif
     if (work->n_items > 0x7fffffffLL - 4 * 128 * 64)
         return fail(FATE_ETOOBIG, "v6: too many items for the 32-bit ticket counter");
     const long long want = (work->n_items + 3) / 4;
@@ -289,6 +305,7 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     return 0;
 }
 
+#ifdef FATE_AB
 template <int DPL, int MINB>
 int launch_v5_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                  const fate_derived* der, const fate_state* st, const fate_work* work,
@@ -304,36 +321,24 @@ int launch_v5_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     return 0;
 }
 
-// register budget: CTAs per SM the register allocation must allow.  Measured
-// on B200 (profiles/): 8 for one device slot per lane (<= 64 registers); for
-// two, 6 (<= 80) for v4/v5 and 7 (<= 72, no spills) for v6.  FATE_MINB =
-// 1 | 6 | 7 | 8 overrides for A/B runs.
-int v5_minb(int dpl) {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("FATE_MINB");
-        v = e ? atoi(e) : 0;
-    }
-    return v ? v : (dpl == 1 ? 8 : 6);
-}
-
 template <int DPL>
 int launch_v5(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
               const fate_derived* der, const fate_state* st, const fate_work* work,
               const fate_out* out, cudaStream_t s) {
-    switch (v5_minb(DPL)) {
+    switch (ab_env("FATE_MINB", DPL == 1 ? 8 : 6, 1, 16)) {
         case 1: return launch_v5_mb<DPL, 1>(bank, w, win, der, st, work, out, s);
         case 6: return launch_v5_mb<DPL, 6>(bank, w, win, der, st, work, out, s);
         default: return launch_v5_mb<DPL, 8>(bank, w, win, der, st, work, out, s);
     }
 }
+#endif
 
-// Lean instantiation (QG = false) when the caller declares that no query has a
+// Lean instantiation (QG = false) when the bank declares that no query has a
 // prefix group (FATE_BANK_NO_QGROUPS) and every device has the same speed
-// (FATE_BANK_UNIFORM_SPEED), and the topology has no transfer override: the
-// per-device query-group and per-speed class paths compile out (configs 4/5:
-// 12 % less code, C4 -6.6 %, C5 -1.7 % on B200 -- the D = 64 kernel was
-// instruction-fetch bound).
+// (FATE_BANK_UNIFORM_SPEED) -- both verified by fate_prepare -- and the
+// topology has no transfer override: the per-device query-group and
+// per-speed class paths compile out (configs 4/5: 12 % less code, C4 -6.6 %,
+// C5 -1.7 % on B200 -- the D = 64 kernel was instruction-fetch bound).
 template <int DPL, bool SL, int MINB>
 int launch_v6_q(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                 const fate_derived* der, const fate_state* st, const fate_work* work,
@@ -345,46 +350,40 @@ int launch_v6_q(const fate_bank* bank, const fate_weights* w, const fate_windows
     return launch_v6_mb<DPL, false, SL, MINB, true>(bank, w, win, der, st, work, out, s);
 }
 
+// Register budget (CTAs per SM), measured on B200: 10 for one device slot per
+// lane (48 registers: the extra warps hide more latency than the spills
+// cost; 8/9/12 were slower), 8 for two (64 registers; 1 % ahead of 7 x 72
+// registers once the chunked op buffer let 8 CTAs fit in shared memory).
 template <int DPL, bool SL>
 int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                  const fate_derived* der, const fate_state* st, const fate_work* work,
                  const fate_out* out, cudaStream_t s) {
-    const char* e = getenv("FATE_MINB");
-    // register budget (CTAs per SM), measured on B200: 10 for one device slot
-    // per lane (48 registers: the extra warps hide more latency than the
-    // spills cost; 8/9/12 were slower), 8 for two (64 registers; 1 % ahead of
-    // 7 x 72 registers once the chunked op buffer let 8 CTAs fit in shared
-    // memory).  FATE_MINB = 7 | 8 | 10 selects another instantiation (A/B).
-    switch (e ? atoi(e) : (DPL == 1 ? 10 : 8)) {
+    constexpr int MINB = DPL == 1 ? 10 : 8;
+#ifdef FATE_AB
+    switch (ab_env("FATE_MINB", MINB, 1, 16)) {
         case 7: return launch_v6_q<DPL, SL, 7>(bank, w, win, der, st, work, out, s);
+        case 8: return launch_v6_q<DPL, SL, 8>(bank, w, win, der, st, work, out, s);
         case 10: return launch_v6_q<DPL, SL, 10>(bank, w, win, der, st, work, out, s);
-        default: return launch_v6_q<DPL, SL, 8>(bank, w, win, der, st, work, out, s);
+        default: break;
     }
+#endif
+    return launch_v6_q<DPL, SL, MINB>(bank, w, win, der, st, work, out, s);
 }
 
 // Static shared-memory layout when the query batch fits it (V6Static<DPL>;
-// measured: C4 -4.5 %).  FATE_V6_DYNLAYOUT forces the runtime layout (A/B).
+// measured: C4 -4.5 %); larger batches use the runtime layout.
 template <int DPL>
 int launch_v6(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
               const fate_derived* der, const fate_state* st, const fate_work* work,
               const fate_out* out, cudaStream_t s) {
+#ifdef FATE_AB
     static const bool dyn = getenv("FATE_V6_DYNLAYOUT") != nullptr;
+#else
+    constexpr bool dyn = false;
+#endif
     if (!dyn && bank->max_queries <= V6Static<DPL>::B)
         return launch_v6_sl<DPL, true>(bank, w, win, der, st, work, out, s);
     return launch_v6_sl<DPL, false>(bank, w, win, der, st, work, out, s);
-}
-
-// Kernel generation: v6 (production) needs the stage records and op templates
-// of fate_prepare; without them -- or with FATE_SCORE_KERNEL=v5 (A/B only) --
-// the previous production kernel v5 runs.  Generations v1-v4 live in the git
-// history (profiles/README.md has their measurements).
-int kernel_gen() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("FATE_SCORE_KERNEL");
-        v = (e && strcmp(e, "v5") == 0) ? 5 : 6;
-    }
-    return v;
 }
 
 int check_bank(const fate_bank* b) {
@@ -399,11 +398,31 @@ int check_bank(const fate_bank* b) {
 
 int check_weights(const fate_weights* w, const fate_windows* win) {
     if (!w || !win) return fail(FATE_EINVAL, "weights/windows is NULL");
+    const double* f = &w->lambda_q;  // the 17 leading doubles of ScoreWeights
+    for (int i = 0; i < 17; ++i)
+        if (!std::isfinite(f[i])) return fail(FATE_EINVAL, "non-finite ScoreWeights field");
+    for (int l = 0; l < FATE_MAX_HORIZON && l < w->eff_horizon + 1; ++l)
+        if (!std::isfinite(w->gamma_pow[l])) return fail(FATE_EINVAL, "non-finite gamma ** l");
     if (w->eff_horizon < 0 || w->eff_horizon >= FATE_MAX_HORIZON)
         return fail(FATE_ETOOBIG, "horizon exceeds FATE_MAX_HORIZON-1");
     const int levels = w->eff_horizon > 1 ? w->eff_horizon - 1 : 0;
     if (win->levels != levels) return fail(FATE_EINVAL, "windows built for another horizon");
     return 0;
+}
+
+// fate_prepare's verification of what the bank declares (the lean kernel
+// instantiation relies on both): FATE_BANK_NO_QGROUPS => every q_group is -1
+// (status bit 1), FATE_BANK_UNIFORM_SPEED => every dev_speed equals device
+// 0's (bit 2).
+__global__ void fate_validate_bank_kernel(fate_bank b, int* status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int stride = gridDim.x * blockDim.x;
+    if (b.flags & FATE_BANK_NO_QGROUPS)
+        for (int q = i; q < b.n_queries; q += stride)
+            if (b.q_group[q] != -1) atomicOr(status, 1);
+    if (b.flags & FATE_BANK_UNIFORM_SPEED)
+        for (int d = i; d < b.n_devices; d += stride)
+            if (b.dev_speed[d] != b.dev_speed[0]) atomicOr(status, 2);
 }
 
 // Wire format -> SoA (fate_pipeline.cpp): blocks [0, n_s) scatter one scenario
@@ -499,6 +518,11 @@ int fate_internal_unpack(const void* rec, size_t rec_bytes, int s0, int s1, int 
     return cuda_status("fate_unpack_kernel");
 }
 
+namespace {
+int prepare(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+            const fate_derived* out, cudaStream_t s);
+}
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -519,6 +543,33 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
     if (rc) return rc;
     if (!out) return fail(FATE_EINVAL, "derived is NULL");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    nvtxRangePushA("fate_prepare");
+    rc = prepare(bank, w, win, out, s);
+    nvtxRangePop();
+    return rc;
+}
+
+}  // extern "C"
+
+namespace {
+
+int prepare(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
+            const fate_derived* out, cudaStream_t s) {
+    int rc = 0;
+    // verification status of the declared bank flags and the op values,
+    // read back once at the end (fate_prepare runs once per (bank, weights))
+    int* status = nullptr;
+    cudaError_t ce = cudaMallocAsync(reinterpret_cast<void**>(&status), sizeof(int), s);
+    if (ce != cudaSuccess) return cuda_status("fate_prepare: status buffer");
+    cudaMemsetAsync(status, 0, sizeof(int), s);
+    struct Free {
+        int* p;
+        cudaStream_t s;
+        ~Free() { cudaFreeAsync(p, s); }
+    } free_status{status, s};
+    fate_validate_bank_kernel<<<1, 128, 0, s>>>(*bank, status);
+    g_launches++;
+    if ((rc = cuda_status("fate_validate_bank_kernel"))) return rc;
     {
         // the v6 quotient tables, once per device (stream-ordered before any
         // scoring launch that follows this prologue)
@@ -562,7 +613,7 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
             if ((rc = cuda_status("fate_prepare_demand_kernel"))) return rc;
             if (out->tmpl && out->tmpl_ptr) {
                 fate_template_fill_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0,
-                                            s>>>(*bank, *w, *win, *out);
+                                            s>>>(*bank, *w, *win, *out, status);
                 g_launches++;
                 if ((rc = cuda_status("fate_template_fill_kernel"))) return rc;
             }
@@ -582,8 +633,23 @@ int fate_prepare(const fate_bank* bank, const fate_weights* w, const fate_window
             }
         }
     }
+    int h = 0;
+    if ((ce = cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (ce = cudaStreamSynchronize(s)) != cudaSuccess)
+        return cuda_status("fate_prepare: status read-back");
+    if (h & 1)
+        return fail(FATE_EINVAL, "bank declares FATE_BANK_NO_QGROUPS but a query has a prefix group");
+    if (h & 2)
+        return fail(FATE_EINVAL, "bank declares FATE_BANK_UNIFORM_SPEED but device speeds differ");
+    if (h & FATE_PREP_NONFINITE)
+        return fail(FATE_EINVAL, "non-finite tail op value (weights x catalog): the exact walk "
+                                 "needs finite op values");
     return 0;
 }
+
+}  // namespace
+
+extern "C" {
 
 int fate_template_count(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                         const fate_derived* der, int64_t* counts, void* stream) {
@@ -615,14 +681,19 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
     if (work->n_items <= 0) return 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int D = bank->n_devices;
-    const bool v6_ready = der->stage_rec && (win->levels == 0 || (der->tmpl_ptr && der->tmpl));
-    if (kernel_gen() == 6 && v6_ready) {
-        rc = D <= 32 ? launch_v6<1>(bank, w, win, der, st, work, out, s)
-                     : launch_v6<2>(bank, w, win, der, st, work, out, s);
-    } else {
+#ifdef FATE_AB
+    // A/B build only: FATE_SCORE_KERNEL=v5 runs the previous generation
+    static const bool v5 = getenv("FATE_SCORE_KERNEL") && !strcmp(getenv("FATE_SCORE_KERNEL"), "v5");
+    if (v5) {
         rc = D <= 32 ? launch_v5<1>(bank, w, win, der, st, work, out, s)
                      : launch_v5<2>(bank, w, win, der, st, work, out, s);
+        if (rc) return rc;
+        g_launches++;
+        return cuda_status("fate_score_kernel");
     }
+#endif
+    rc = D <= 32 ? launch_v6<1>(bank, w, win, der, st, work, out, s)
+                 : launch_v6<2>(bank, w, win, der, st, work, out, s);
     if (rc) return rc;
     g_launches++;
     return cuda_status("fate_score_kernel");

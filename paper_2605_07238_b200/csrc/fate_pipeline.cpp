@@ -28,6 +28,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "fate.h"
 #include "fate_internal.h"
 
@@ -260,8 +262,13 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
     }
     bounds.push_back(W);
 
-    // FATE_PIPE_TRACE=1: per-chunk timeline on stderr (diagnostic; synchronizes)
+    // FATE_PIPE_TRACE=1 (-DFATE_AB experiment builds only): per-chunk timeline
+    // on stderr (diagnostic; synchronizes)
+#ifdef FATE_AB
     static const bool trace_env = getenv("FATE_PIPE_TRACE") != nullptr;
+#else
+    constexpr bool trace_env = false;
+#endif
     const bool trace = trace_env && !capturing;
     std::vector<cudaEvent_t> tev;
     const auto mark = [&](cudaStream_t st) {
@@ -314,6 +321,7 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
     }
     cudaStream_t sh = p->streams[0], sd = p->streams[1];
     const auto comp = [&](size_t c) { return p->streams[2 + c % (p->streams.size() - 2)]; };
+    nvtxRangePushA("fate_pipeline:h2d");
     for (size_t c = 0; c < ch.size(); ++c) {
         const Chunk& k = ch[c];
         const Copy h2d[] = {
@@ -332,6 +340,8 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
         if ((e = cudaEventRecord(p->in_ready[c], sh)) != cudaSuccess)
             return cuda_fail(e, "fate_pipeline_score: H2D event");
     }
+    nvtxRangePop();
+    nvtxRangePushA("fate_pipeline:score");
     for (size_t c = 0; c < ch.size(); ++c) {
         const Chunk& k = ch[c];
         cudaStream_t s = comp(c);
@@ -362,6 +372,8 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
         if ((e = cudaEventRecord(p->scored[c], s)) != cudaSuccess)
             return cuda_fail(e, "fate_pipeline_score: score event");
     }
+    nvtxRangePop();
+    nvtxRangePushA("fate_pipeline:d2h");
     for (size_t c = 0; c < ch.size(); ++c) {
         const Chunk& k = ch[c];
         const size_t ni = (size_t)(k.i1 - k.i0);
@@ -383,6 +395,7 @@ int enqueue(fate_pipeline* p, const fate_bank* bank, const fate_weights* w,
         }
         mark(sd);
     }
+    nvtxRangePop();
     if (trace) {
         cudaDeviceSynchronize();
         fprintf(stderr, "[fate_pipeline] chunk: h2d_end unpack_start score_start score_end d2h_end (us)\n");

@@ -271,12 +271,22 @@ __global__ void fate_template_count_kernel(fate_bank b, fate_weights w, fate_win
     counts[vl] = v6_template_walk(b, w, win, der, vl, nullptr);
 }
 
+// status bit FATE_PREP_NONFINITE: an op value is not finite.  The walk applies
+// a skipped op as fma(v, +0.0, a), which equals a only for finite v (the
+// reference never evaluates a skipped op), so such a bank is rejected.
+constexpr int FATE_PREP_NONFINITE = 4;
+
 __global__ void fate_template_fill_kernel(fate_bank b, fate_weights w, fate_windows win,
-                                          fate_derived der) {
+                                          fate_derived der, int* status) {
     const long long vl = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (vl >= (long long)b.n_stages * win.levels) return;
-    v6_template_walk(b, w, win, der, vl,
-                     reinterpret_cast<V6Op*>(der.tmpl) + der.tmpl_ptr[vl]);
+    V6Op* out = reinterpret_cast<V6Op*>(der.tmpl) + der.tmpl_ptr[vl];
+    const long long n = v6_template_walk(b, w, win, der, vl, out);
+    for (long long i = 0; i < n; ++i)
+        if (!isfinite(out[i].val)) {
+            atomicOr(status, FATE_PREP_NONFINITE);
+            break;
+        }
 }
 
 // ---------------------------------------------------------------------------

@@ -270,3 +270,26 @@ def test_c_abi_from_plain_c(tmp_path):
     assert int(fields["optimal"]) == int(want.optimal)
     assert int(fields["nodes"]) == want.nodes_explored
     assert int(fields["abi"]) == runtime.load_library().fate_abi_version()
+
+
+def test_production_library_has_one_kernel_generation():
+    """Without -DFATE_AB the library carries the v6 scoring kernel only (no
+    v5 A/B generation) and no environment knobs."""
+    import shutil
+    import subprocess
+
+    if not os.path.exists(runtime.LIB_PATH) or shutil.which("cuobjdump") is None:
+        pytest.skip("libfate.so or cuobjdump missing")
+    from paper_2605_07238_b200 import build
+
+    if build.ab_build():
+        pytest.skip("experiment build")
+    names = subprocess.run(["cuobjdump", "-symbols", runtime.LIB_PATH], capture_output=True,
+                           text=True).stdout
+    assert "fate_score_v6_kernel" in names
+    assert "fate_score_v5_kernel" not in names
+    with open(runtime.LIB_PATH, "rb") as fh:
+        blob = fh.read()
+    for knob in (b"FATE_SCORE_KERNEL", b"FATE_MINB", b"FATE_V6_OPCAP", b"FATE_V6_FETCH",
+                 b"FATE_PIPE_TRACE", b"FATE_V6_DYNLAYOUT"):
+        assert knob not in blob, knob
