@@ -261,6 +261,25 @@ int fate_score(const fate_bank* bank, const fate_weights* w, const fate_windows*
                const fate_derived* der, const fate_state* st, const fate_work* work,
                const fate_out* out, void* stream);
 
+/* ---- executor-side realized durations ------------------
+ * CostModel.realized_duration(stage, [(device, queries)], state)
+ * (costs.py:383-416) of n_tasks independent shard tasks on scenario `scen` of
+ * a fate_state (e.g. the device-resident mirror of the running instance):
+ * timing[3*i .. 3*i+2] = (switch_s, transfer_s, compute_s) of task i, whose
+ * queries are the instance-local query indices task_queries[q0 .. q0+nq) in
+ * order (compute_s is their CPython sum).  Device pointers; the caller
+ * validates eligibility and disjointness (costs.py:391-401) on the host. */
+typedef struct fate_task {
+    int32_t stage;                  /* global stage index */
+    int32_t device;
+    int32_t q0;
+    int32_t nq;
+} fate_task;
+
+int fate_realized(const fate_bank* bank, const fate_weights* w, const fate_state* st,
+                  int32_t scen, int32_t n_tasks, const fate_task* tasks,
+                  const int32_t* task_queries, double* timing, void* stream);
+
 /* ---- host frontier solve -------------------------------
  * Native restatement of wfsched.planner.solve_frontier with its front half
  * _stage_options and the deadline fallback _greedy_fallback

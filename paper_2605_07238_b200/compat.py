@@ -79,9 +79,10 @@ def install(scorer=None, policy_factory: bool = True, mirror=None,
             if hasattr(mod, "make_policy"):
                 _set(mod, "make_policy", make_policy)
     if durations:
-        from .durations import GpuCostModel
+        from . import durations as dur
 
-        _set(ex, "CostModel", GpuCostModel)
+        dur.set_source(mirror if mirror is not None else scorer)
+        _set(ex, "CostModel", dur.GpuCostModel)
     if mirror is not None:
         real_state = ex.ExecutionState
         real_ready = ex.ready_set
@@ -109,5 +110,9 @@ def install(scorer=None, policy_factory: bool = True, mirror=None,
 def uninstall() -> None:
     for (mod, name), value in _saved.items():
         setattr(mod, name, value)
+    if _bound.get("durations"):
+        from . import durations as dur
+
+        dur.set_source(None)
     _saved.clear()
     _bound.clear()

@@ -410,6 +410,61 @@ int check_weights(const fate_weights* w, const fate_windows* win) {
     return 0;
 }
 
+// realized_duration (costs.py:383-416) of arbitrary shard tasks on one
+// scenario state, one thread per task: switch_cost (costs.py:107-111),
+// transfer_cost (costs.py:113-125, beta table), and the CPython-sum of the
+// cache-aware query_compute (costs.py:70-94) over the task's queries in their
+// order -- the executor's issue-time pricing (executor.py:231-233).
+__global__ void fate_realized_kernel(fate_bank b, fate_weights w, fate_state st, int scen, int n,
+                                     const fate_task* __restrict__ tasks,
+                                     const int32_t* __restrict__ tq, double* __restrict__ timing) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const fate_task t = tasks[i];
+    const int v = t.stage, d = t.device, D = b.n_devices;
+    const int inst = b.st_inst[v];
+    const int m = b.st_model[v], r = b.st_role[v];
+    const long long row = (long long)scen * D + d;
+    const double sw = (m < 0 || st.residency[row] == m) ? 0.0 : b.model_switch[m] * w.switch_x;
+    const int32_t* loc_row = st.loc + st.scen_loc_off[scen] - b.inst_stage_off[inst];
+    const double comm = b.role_comm[r];
+    double tr = 0.0;
+    for (int e = b.par_ptr[v]; e < b.par_ptr[v + 1]; ++e) {
+        const int u = b.par_idx[e];
+        const int L = loc_row[u];
+        if (L < 0 || L == d) continue;
+        const double sigma = (double)b.st_out[u] * comm / 1000.0;
+        tr += b.beta[(size_t)L * D + d] * sigma;
+    }
+    tr = tr * w.transfer_x;
+    const double pcoef = m >= 0 ? b.model_prefill[m] : 1.0;
+    const double dcoef = m >= 0 ? b.model_decode[m] : 0.0;
+    const double decode = (double)b.st_out[v] * dcoef * b.role_decode[r];
+    const int32_t* kap = st.kappa + row * st.kappa_cap * 4;
+    const int kn = st.kappa_n[row];
+    long long sp = b.st_prompt[v];
+    const int gv = b.st_group[v];
+    if ((b.st_flags[v] & FATE_STAGE_CACHE_REUSE) && gv != -1) {
+        const long long c = cached_tokens(kap, kn, gv, m);
+        sp = sp - c > 0 ? sp - c : 0;
+    }
+    const int q0 = b.inst_query_off[inst];
+    PySum acc;
+    for (int k = t.q0; k < t.q0 + t.nq; ++k) {
+        const int q = q0 + tq[k];
+        long long qp = b.q_prompt[q];
+        if (b.q_group[q] != -1) {
+            const long long c = cached_tokens(kap, kn, b.q_group[q], m);
+            qp = qp - c > 0 ? qp - c : 0;
+        }
+        acc.add(qc_value(sp, qp, pcoef, b.role_prefill[r], decode, b.role_cplx[r],
+                         b.dev_speed[d]));
+    }
+    timing[3 * i + 0] = sw;
+    timing[3 * i + 1] = tr;
+    timing[3 * i + 2] = acc.result();
+}
+
 // fate_prepare's verification of what the bank declares (the lean kernel
 // instantiation relies on both): FATE_BANK_NO_QGROUPS => every q_group is -1
 // (status bit 1), FATE_BANK_UNIFORM_SPEED => every dev_speed equals device
@@ -650,6 +705,23 @@ int prepare(const fate_bank* bank, const fate_weights* w, const fate_windows* wi
 }  // namespace
 
 extern "C" {
+
+int fate_realized(const fate_bank* bank, const fate_weights* w, const fate_state* st,
+                  int32_t scen, int32_t n_tasks, const fate_task* tasks,
+                  const int32_t* task_queries, double* timing, void* stream) {
+    int rc = check_bank(bank);
+    if (rc) return rc;
+    if (!w || !st || (n_tasks > 0 && (!tasks || !task_queries || !timing)))
+        return fail(FATE_EINVAL, "fate_realized: NULL argument");
+    if (scen < 0 || scen >= st->n_scenarios || n_tasks < 0)
+        return fail(FATE_EINVAL, "fate_realized: scenario or task count out of range");
+    if (n_tasks == 0) return 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    fate_realized_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(*bank, *w, *st, scen, n_tasks,
+                                                                tasks, task_queries, timing);
+    g_launches++;
+    return cuda_status("fate_realized_kernel");
+}
 
 int fate_template_count(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                         const fate_derived* der, int64_t* counts, void* stream) {

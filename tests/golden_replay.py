@@ -155,18 +155,21 @@ def record_mismatches(rec, want: dict) -> list:
 
 
 def replay(run_meta: dict, arrays: dict, instance, config, scorer, seed: int = 0,
-           solver: str = "reference", mirror=None):
+           solver: str = "reference", mirror=None, durations: bool = False):
     """One FATE run of the reference executor with the GPU policy; ``mirror``
-    (a MirrorScorer) is attached to the executor's live state through
-    ``compat.install(mirror=...)``."""
+    (a MirrorScorer) is attached to the executor's live state and
+    ``durations`` prices the executor's issued tasks on the GPU, both through
+    ``compat.install``."""
     chk = CheckingScorer(scorer, run_meta, arrays)
     policy = FateGpuPolicy(scorer=chk, solver=solver)
-    if mirror is not None:
-        compat.install(mirror=mirror, policy_factory=False)
+    hooked = mirror is not None or durations
+    if hooked:
+        compat.install(scorer=None if mirror is not None else scorer, mirror=mirror,
+                       policy_factory=False, durations=durations)
     try:
         rec = RE.run(policy, instance, config, seed=seed)
     finally:
-        if mirror is not None:
+        if hooked:
             compat.uninstall()
     problems = list(chk.mismatches)
     if chk.i != len(run_meta["waves"]):

@@ -121,3 +121,63 @@ def test_mirror_reports_prefix_overflow_and_bad_events():
     with pytest.raises(ValueError):
         m.ready()
     m.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c2"])
+@pytest.mark.parametrize("with_mirror", [True, False])
+def test_executor_issue_durations_on_gpu(name, with_mirror):
+    """the reference executor prices every issued task
+    with the GPU (durations.GpuCostModel via compat.install(durations=True)),
+    from the device mirror of its live state or from a packed upload; every
+    wave and RunRecord still equals the captured reference run."""
+    from paper_2605_07238_b200.planner import GpuScorer
+
+    runs, arrs = G.load(name)
+    if name == "c2":
+        runs = runs[::12]
+    bad = []
+    for r in runs:
+        if name == "c1":
+            inst, cfg = G.c1_setup(r["variant"])
+        elif name == "c2":
+            inst, cfg = G.c2_setup(r["key"])
+        else:
+            inst, cfg = G.c3_setup(r["ratio"], r["batch"], r["shape"])
+        scorer = MirrorScorer() if with_mirror else GpuScorer()
+        _, problems, _ = G.replay(r, arrs, inst, cfg, scorer,
+                                  mirror=scorer if with_mirror else None, durations=True)
+        if problems:
+            bad.append(problems[:3])
+    assert not bad, bad
+
+
+def test_gpu_realized_duration_equals_reference_on_shards():
+    """fate_realized against the reference CostModel.realized_duration on
+    multi-shard assignments (partial query sets, every eligible device) over
+    the canonical config-5 scenario states."""
+    import wfsched.costs as RC
+
+    from paper_2605_07238_b200 import durations, scenarios
+    from paper_2605_07238_b200.planner import GpuScorer
+
+    cfg = scenarios.config_c5()
+    durations.set_source(GpuScorer())
+    try:
+        for i in range(3):
+            inst = scenarios.c5_instance(i, cfg)
+            st = scenarios.build_scenario(inst, cfg, i)
+            ref = RC.CostModel(cfg.models, cfg.topology, cfg.weights)
+            gpu = durations.GpuCostModel(cfg.models, cfg.topology, cfg.weights)
+            qids = tuple(q.query_id for q in inst.queries)
+            for sid in sorted(inst.dag.stages)[::37]:
+                stage = inst.dag.stages[sid]
+                devs = sorted(stage.eligible_devices)
+                shards = [(devs[0], qids[:5]), (devs[-1], qids[5:11]), (devs[3], qids[11:])]
+                want = ref.realized_duration(stage, shards, st, inst.dag)
+                got = gpu.realized_duration(stage, shards, st, inst.dag)
+                assert [(t.switch_s.hex(), t.transfer_s.hex(), t.compute_s.hex()) for t in got] == \
+                    [(t.switch_s.hex(), t.transfer_s.hex(), t.compute_s.hex()) for t in want], sid
+                with pytest.raises(ValueError):
+                    gpu.realized_duration(stage, [(devs[0], qids[:3]), (devs[1], qids[2:4])], st)
+    finally:
+        durations.set_source(None)

@@ -388,3 +388,32 @@ def test_c4_full_sweep_scenario_and_c5_full_frontier():
     d5 = runtime.DeviceBank(fb.bank, cfg5.weights)
     got5 = d5.score(fb.states, work5, extras=False).psi.cpu().numpy()[: work5.n_psi]
     assert np.array_equal(bits(got5), bits(want5))
+
+
+def test_prepare_rejects_false_bank_declarations_and_nonfinite_ops():
+    """fate_prepare verifies what a bank declares (FATE_BANK_NO_QGROUPS,
+    FATE_BANK_UNIFORM_SPEED -- the lean kernel relies on both) and that every
+    tail op value is finite (the exact walk's skipped op is fma(v, 0, a)):
+    a false declaration or a non-finite weight is a status < 0, not wrong Psi."""
+    import copy
+
+    case = small_case()
+    qg = copy.deepcopy(case.bank)
+    qg.arrays["q_group"] = qg.arrays["q_group"].copy()
+    qg.arrays["q_group"][0] = 0
+    qg.scalars["flags"] |= pack.BANK_NO_QGROUPS
+    with pytest.raises(ValueError, match="NO_QGROUPS"):
+        runtime.DeviceBank(qg, case.weights)
+    sp = copy.deepcopy(case.bank)
+    sp.arrays["dev_speed"] = sp.arrays["dev_speed"].copy()
+    sp.arrays["dev_speed"][-1] = 1.5
+    sp.scalars["flags"] |= pack.BANK_UNIFORM_SPEED
+    with pytest.raises(ValueError, match="UNIFORM_SPEED"):
+        runtime.DeviceBank(sp, case.weights)
+    with pytest.raises(ValueError, match="non-finite"):
+        runtime.DeviceBank(case.bank, replace(case.weights, switch_x=float("inf")))
+    big = replace(case.weights, switch_x=1e308, state_scale=1e308)  # finite weights, inf ops
+    if any(float(case.bank.arrays["model_switch"][m]) > 0 for m in range(len(case.bank.arrays["model_switch"]))):
+        with pytest.raises(ValueError, match="non-finite"):
+            runtime.DeviceBank(case.bank, big)
+    runtime.DeviceBank(case.bank, case.weights)  # the honest bank still prepares
