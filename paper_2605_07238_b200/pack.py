@@ -529,6 +529,90 @@ def compulsory_bytes(bank: PackedBank, work: WorkList, states: PackedStates, lev
     return int(math.floor(total + 0.5))
 
 
+# per (item, eligible device): the fp64 operations the reference's formulas
+# mandate outside the tail walk -- sched_score (costs.py:222-231: 10 products,
+# 5 sums, 1 negation), Psi(slot 0) = S + tail, wait, completion (3), prefix
+# (2), the tail's per-level combination (5 per nonempty level: divide,
+# product, sum, gamma product, accumulate), _parallel_benefit when R > 1 (6)
+# and each slot >= 1 of _marginal_shard_score (15).  Divisions count as one
+# operation (a lower bound).
+FP64_PER_CAND_FIXED = 16 + 1 + 1 + 3 + 2
+FP64_PER_LEVEL = 5
+FP64_PARALLEL = 6
+FP64_MARGINAL = 15
+
+
+def mandated_fp64_ops(bank: PackedBank, work: WorkList, states: PackedStates, levels: int,
+                      windows, sample: int = 3000, seed: int = 0) -> dict:
+    """Lower bound on the fp64 operations a scoring launch must execute,
+    estimated on a uniform sample of its work items and scaled to the launch:
+    the fixed per-candidate arithmetic above plus, for every horizon level with
+    a located window parent (the only levels whose chain is state-dependent),
+    one add per (op, device it applies to) of the tail's op sequence
+    (costs.py:307-348: model op, prefix op, located parent edges other than v).
+    Sequential += chains cannot be shared between devices whose op sequences
+    differ, so each is an fp64 add per device."""
+    a = bank.arrays
+    D = bank.scalars["n_devices"]
+    M = bank.scalars["n_models"]
+    rng = np.random.default_rng(seed)
+    n = work.n_items
+    pick = np.arange(n) if n <= sample else np.sort(rng.choice(n, sample, replace=False))
+    par_ptr, par_idx = a["par_ptr"], a["par_idx"]
+    st_model, st_group, st_level = a["st_model"], a["st_group"], a["st_level"]
+    ptr, idx = windows if levels else (None, None)
+    S = states.arrays
+    tot = 0.0
+    walk_tot = 0.0
+    for w in pick:
+        s, v = int(work.scen[w]), int(work.stage[w])
+        elig = int(a["st_elig"][v])
+        ne = bin(elig).count("1")
+        bound = int(work.bounds[w])
+        n_lev = 0
+        walk = 0.0
+        if levels:
+            inst = int(a["st_inst"][v])
+            off = int(S["scen_loc_off"][s]) - int(bank.inst_stage_off[inst])
+            res = S["residency"][s * D:(s + 1) * D]
+            mv = int(st_model[v])
+            disp = np.array([(r if (r != -1 and r != mv and r < M) else -1) for r in res])
+            cls = {x: int(np.sum((disp == x) & np.array([(elig >> d) & 1 for d in range(D)],
+                                                        dtype=bool))) for x in range(M)}
+            for l in range(levels):
+                lo, hi = int(ptr[v * levels + l]), int(ptr[v * levels + l + 1])
+                if hi == lo:
+                    continue
+                n_lev += 1
+                xs = idx[lo:hi]
+                ops = 0.0
+                located = False
+                for x in xs:
+                    mx = int(st_model[x])
+                    if mx != -1:
+                        ops += ne if mx == mv else cls.get(mx, 0)
+                    if st_group[v] != -1 and st_group[x] == st_group[v]:
+                        ops += ne
+                    for e in range(int(par_ptr[x]), int(par_ptr[x + 1])):
+                        u = int(par_idx[e])
+                        if u == v:
+                            continue
+                        L = int(S["loc"][off + u])
+                        if L >= 0:
+                            located = True
+                            ops += ne - ((elig >> L) & 1)
+                if located:
+                    walk += ops
+        fixed = ne * (FP64_PER_CAND_FIXED + FP64_PER_LEVEL * n_lev
+                      + (FP64_PARALLEL if int(a["st_shard"][v]) > 1 else 0)
+                      + FP64_MARGINAL * max(0, bound - 1))
+        tot += fixed + walk
+        walk_tot += walk
+    scale = n / max(1, len(pick))
+    return {"fp64_ops": tot * scale, "walk_adds": walk_tot * scale,
+            "sampled_items": int(len(pick)), "items": int(n)}
+
+
 # ---------------------------------------------------------------------------
 # host wire format of fate_pipeline_score (include/fate.h: fate_host_batch)
 # ---------------------------------------------------------------------------

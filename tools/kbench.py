@@ -1,0 +1,41 @@
+"""Kernel-only A/B timing: C5 frontier and C4 sweep, CUDA events around each
+scoring launch, L2 flushed between steps (bench.py's time_device).  Prints
+one JSON line.  usage: python tools/kbench.py [steps] [reps]"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main():
+    import torch
+
+    from paper_2605_07238_b200 import runtime
+
+    steps = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    dev = torch.device("cuda:0")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    out = {"lib": os.environ.get("KB_TAG", "")}
+    for name, build in (("c5", lambda: bench.build_c5(bench.shard_plan(0, 1), "frontier")),
+                        ("c4", lambda: bench.build_c4("sweep"))):
+        cfg, bank, states, work = build()
+        db = runtime.DeviceBank(bank, cfg.weights, device=dev)
+        ds, dw = db.upload_states(states), db.upload_work(work)
+        o = db.alloc_out(work, extras=True)
+        o.tail = None
+        ms = []
+        for _ in range(reps):
+            m, _ = bench.time_device(torch, db, ds, dw, o, steps, 5, flush, 1, dev)
+            ms.append(m)
+        out[name + "_ms"] = sorted(ms)[len(ms) // 2]
+        out[name + "_all"] = ms
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
