@@ -157,6 +157,11 @@ typedef struct fate_work {
     const int32_t* scen;            /* [W] */
     const int32_t* stage;           /* [W] global stage index */
     const int64_t* psi_off;         /* [W] first psi entry of the item */
+    /* optional: the work list's own ticket counter (2 x uint32, zero on
+     * creation; each launch leaves it zero again).  Launches of different
+     * work lists then never share a counter however many are in flight;
+     * NULL = the library's rotating counters (128 direct-launch slots). */
+    uint32_t* queue;
 } fate_work;
 
 /* Horizon windows: descendants of each stage bucketed by level offset

@@ -60,7 +60,7 @@ class FateHostBatch(C.Structure):
 
 class FateWork(C.Structure):
     _fields_ = [("n_items", C.c_int32), ("reserved", C.c_int32), ("scen", _p), ("stage", _p),
-                ("psi_off", _p)]
+                ("psi_off", _p), ("queue", _p)]
 
 
 class FateWindows(C.Structure):

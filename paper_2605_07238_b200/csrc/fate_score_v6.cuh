@@ -1153,10 +1153,13 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 // with the number of walked horizon levels, and consecutive items -- stages
 // of one scenario in index order -- have correlated costs).  Each launch uses
 // its own counter slot and the last warp of a launch resets the slot to zero,
-// so a captured graph replays without a reset node.  Slots [0, V6_QDIRECT)
-// rotate over direct fate_score calls; the rest are reserved per host
-// pipeline compute stream (fate_internal_reserve_queue_slot), so a captured
-// pipeline graph never shares a counter with a concurrent direct launch.
+// so a captured graph replays without a reset node.  A work list may bring
+// its own counter (fate_work.queue; runtime.DeviceWork passes one per
+// (work list, stream)), so launches in flight never share one however many
+// there are.  Without it: slots [0, V6_QDIRECT) rotate over direct
+// fate_score calls; the rest are reserved per host pipeline compute stream
+// (fate_internal_reserve_queue_slot), so a captured pipeline graph never
+// shares a counter with a concurrent direct launch.
 constexpr int V6_QSLOTS = 256;
 constexpr int V6_QDIRECT = 128;
 __device__ unsigned int g_v6_queue[2 * V6_QSLOTS];  // per slot: next ticket, warps done
@@ -1171,7 +1174,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int t = threadIdx.x & 31;
     const int wi = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-    unsigned int* q = g_v6_queue + 2 * qslot;
+    unsigned int* q = work.queue ? work.queue : g_v6_queue + 2 * qslot;
     const long long n = work.n_items;
     unsigned char* sb = smem_raw + lay.item_bytes * wi;
     // fetch > 0: fixed items per ticket; fetch == 0: guided -- a ticket takes

@@ -320,6 +320,8 @@ class DeviceBank:
             tail=out.tail.data_ptr() if out.tail is not None else None,
             completion=out.completion.data_ptr() if out.completion is not None else None,
             timing=out.timing.data_ptr() if out.timing is not None else None)
+        if hasattr(dwork, "queue_for"):
+            dwork.cwork.queue = dwork.queue_for(s)
         _check(load_library().fate_score(
             C.byref(self.cbank), C.byref(self.cweights), C.byref(self.cwin), C.byref(self.cder),
             C.byref(dstates.cstate), C.byref(dwork.cwork), C.byref(cout),
@@ -355,6 +357,21 @@ class DeviceWork:
             dbank.device, non_blocking=non_blocking) for k in ("scen", "stage", "psi_off")}
         self.cwork = abi.fill_struct(abi.FateWork(), {"n_items": work.n_items},
                                      {k: v.data_ptr() for k, v in self.t.items()})
+        self._torch = torch
+        self._device = dbank.device
+        self._queues: dict = {}
+
+    def queue_for(self, stream) -> int:
+        """This work list's self-resetting ticket counter for launches on
+        ``stream`` (fate_work.queue): launches on one stream are ordered, so a
+        counter per (work list, stream) is never shared by two launches in
+        flight, however many streams and work lists are active."""
+        key = int(stream.cuda_stream)
+        q = self._queues.get(key)
+        if q is None:
+            q = self._queues[key] = self._torch.zeros(2, dtype=self._torch.int32,
+                                                      device=self._device)
+        return q.data_ptr()
 
 
 class HostPipeline:

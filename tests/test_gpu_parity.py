@@ -417,3 +417,29 @@ def test_prepare_rejects_false_bank_declarations_and_nonfinite_ops():
         with pytest.raises(ValueError, match="non-finite"):
             runtime.DeviceBank(case.bank, big)
     runtime.DeviceBank(case.bank, case.weights)  # the honest bank still prepares
+
+
+def test_more_concurrent_launches_than_rotating_counter_slots():
+    """160 launches in flight on 160 streams (more than the library's 128
+    rotating ticket counters): each (work list, stream) brings its own
+    counter (fate_work.queue), so every result equals the oracle."""
+    import torch
+
+    case = c5_case(n_inst=2)
+    want = bits(oracle.score(case.bank, case.wrec, case.states, case.work)["psi"])
+    n = case.work.n_psi
+    dbank = runtime.DeviceBank(case.bank, case.weights)
+    ds, dw = dbank.upload_states(case.states), dbank.upload_work(case.work)
+    outs = [dbank.alloc_out(case.work, extras=False) for _ in range(160)]
+    streams = [torch.cuda.Stream() for _ in outs]
+    gate = torch.cuda.Event()
+    hold = torch.cuda.current_stream()
+    torch.cuda._sleep(20_000_000)  # keep the streams' launches queued together
+    gate.record(hold)
+    for o, s in zip(outs, streams):
+        s.wait_event(gate)
+        dbank.score_into(ds, dw, o, stream=s)
+    torch.cuda.synchronize()
+    assert len(dw._queues) == 160
+    for o in outs:
+        assert np.array_equal(bits(o.psi.cpu().numpy()[:n]), want)
