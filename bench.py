@@ -785,6 +785,11 @@ def run_fate(args):
     c4 = None
     if args.workload == "c5" and not args.no_c4:
         c4 = measure_c4(torch, device, args, rank, world)
+    c2 = None
+    if rank == 0 and world == 1 and args.workload == "c5" and not args.no_c2:
+        nvtx.range_push("c2_fate_runs")
+        c2 = measure_c2_runs()
+        nvtx.range_pop()
 
     items_total = reduce_sum(float(work.n_items), world, device)
     if rank == 0:
@@ -809,11 +814,79 @@ def run_fate(args):
             line["weak"] = weak
         if c4 is not None:
             line["c4_sweep"] = c4
+        if c2 is not None:
+            line["c2_fate_runs"] = c2
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def measure_c2_runs() -> dict | None:
+    """The drop-in at its API: all 96 FATE runs of config 2
+    (the reference's default manifest, main group) through the REFERENCE
+    executor, timed end to end (wall clock, host objects in, RunRecords out)
+    three ways: the reference's own FatePolicy (CPython scorer), FateGpuPolicy
+    scoring each wave's snapshot on the GPU, and FateGpuPolicy on the
+    device-resident state mirror with the GPU ready set and GPU issue-time
+    durations.  Records must be identical."""
+    reference_on_path()
+    try:
+        import wfsched.executor as RE
+        import wfsched.harness as RH
+        import wfsched.policies as RP
+        from wfsched.config import default_config
+    except ImportError:
+        return None
+    from paper_2605_07238_b200 import compat
+    from paper_2605_07238_b200.mirror import MirrorScorer
+    from paper_2605_07238_b200.planner import FateGpuPolicy, GpuScorer
+
+    man = RH.default_manifest()
+    cfg = default_config(man.num_devices)
+    reg = RH.materialize_workloads(man, cfg)
+    keys = sorted(k for k, inst in reg.items()
+                  if inst.dag.family not in ("prefix_reuse", "conflict"))
+
+    def rec_key(r):
+        return (r.makespan.hex(), tuple(sorted((k, v.hex()) for k, v in r.query_completion.items())),
+                r.workflow_tasks, r.cross_device_parent_edges)
+
+    out = {"runs": len(keys)}
+    recs = {}
+    t0 = time.perf_counter()
+    recs["reference"] = [RE.run(RP.make_policy("fate"), reg[k], cfg) for k in keys]
+    out["reference_python_s"] = time.perf_counter() - t0
+    scorer = GpuScorer()
+    pols = []
+    t0 = time.perf_counter()
+    rr = []
+    for k in keys:
+        pol = FateGpuPolicy(scorer=scorer)
+        rr.append(RE.run(pol, reg[k], cfg))
+        pols.append(pol)
+    out["gpu_policy_s"] = time.perf_counter() - t0
+    recs["gpu"] = rr
+    out["waves"] = int(sum(p.solver_stats.solves for p in pols))
+    out["gpu_score_s"] = float(sum(p.score_seconds for p in pols))
+    t0 = time.perf_counter()
+    rr = []
+    for k in keys:
+        m = MirrorScorer(gpu_frontier=True)
+        compat.install(mirror=m, policy_factory=False, durations=True)
+        try:
+            rr.append(RE.run(FateGpuPolicy(scorer=m), reg[k], cfg))
+        finally:
+            compat.uninstall()
+    out["gpu_mirror_durations_s"] = time.perf_counter() - t0
+    recs["mirror"] = rr
+    want = [rec_key(r) for r in recs["reference"]]
+    out["identical_records"] = all([rec_key(r) for r in recs[n]] == want for n in ("gpu", "mirror"))
+    out["note"] = ("wall clock of whole runs (executor, solve, fill, materialise included); "
+                   "median config-2 wave has 16 candidates, so per-wave launch/copy latency, "
+                   "not kernel time, bounds the GPU policies")
+    return out
 
 
 def measure_c4(torch, device, args, rank: int = 0, world: int = 1) -> dict:
@@ -853,6 +926,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-weak", action="store_true")
+    ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-instances", type=int, default=8)
     ap.add_argument("--ref-pool", type=int, default=32)
