@@ -651,7 +651,31 @@ def _roofline(pack, runtime, bank, work, states, dbank, ms, key, sm_mhz):
     ceil = issue_ceiling(key, ms, sm_mhz)
     if ceil is not None:
         roof["issue_ceiling"] = ceil
+    roof["fp64_floor"] = fp64_floor(pack, runtime, bank, work, states, dbank, ms)
     return roof
+
+
+def fp64_floor(pack, runtime, bank, work, states, dbank, ms) -> dict:
+    """Lower bound from the fp64 arithmetic the reference's formulas mandate
+    (pack.mandated_fp64_ops, estimated on a sample of items) at the measured
+    FP64 pipe rate (one warp DADD per two cycles per scheduler,
+    profiles/r01_issue_probe.json): the time the launch would take if it
+    issued nothing but its mandated fp64 operations."""
+    rate = 575.03e9
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_issue_probe.json")) as fh:
+            rate = float(json.load(fh)["dadd_ginst_s"]) * 1e9
+    except Exception:
+        pass
+    est = pack.mandated_fp64_ops(bank, work, states, dbank.levels,
+                                 runtime.build_windows(bank, dbank.levels))
+    floor_ms = est["fp64_ops"] / 32.0 / rate * 1e3
+    return {"fp64_ops_per_launch": est["fp64_ops"], "walk_adds_per_launch": est["walk_adds"],
+            "fp64_ops_per_candidate": est["fp64_ops"] / max(1, work.n_psi),
+            "dadd_warp_inst_per_s": rate, "floor_ms": floor_ms,
+            "floor_over_measured": floor_ms / ms,
+            "estimate": f"{est['sampled_items']} of {est['items']} work items sampled; "
+                        "divisions counted as one op"}
 
 
 def run_fate(args):

@@ -258,10 +258,14 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     const int opcap = v6_opcap_default<DPL>();
 #endif
     constexpr bool maskw = !OVR && DPL == 2;
-    const V6Layout lay =
+    V6Layout lay =
         SL ? v6_layout_static<DPL>(win->max_level_ops, bank->n_models, maskw, opcap)
            : v6_layout(bank->n_devices, bank->max_queries, win->max_level_ops, bank->n_models,
                        maskw, opcap);
+#ifdef FATE_AB
+    static const int diag_env = ab_env("FATE_V6_DIAG", 0, 0, 15);
+    lay.diag = diag_env;
+#endif
     const size_t smem = (size_t)lay.item_bytes * 4;
     if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v6 shared-memory footprint too large");
     if (smem > 48 * 1024)

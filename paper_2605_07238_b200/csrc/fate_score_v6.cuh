@@ -82,6 +82,10 @@ struct V6Layout {
     int item_bytes;
     int rows, shard, aware, sw, tr, opval, opmask, key, cslot, rowdev, mmask;
     int ops_cap;  // op-buffer entries (multiple of 4, >= 32)
+    int diag;     // -DFATE_AB experiment builds only (FATE_V6_DIAG): 1 = skip the
+                  // tail walk, 2 = skip the per-device assembly, 4 = compact the op
+                  // lists but skip their walk, 8 = no location gather in the
+                  // compaction (timing probes; results are then wrong)
 };
 
 // Op buffer: a level's op list is compacted and walked in chunks of at most
@@ -800,6 +804,9 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         dmc[j] = (live[j] && res0[j] != -1 && res0[j] != m && res0[j] < b.n_models) ? res0[j] : -1;
         tgt[j] = dmc[j] >= 0 ? V6_KEY_MODEL + dmc[j] : -2;
     }
+#ifdef FATE_AB
+    if (lay.diag & 1) walk_m = 0u;
+#endif
     if (do_tail && walk_m == 0u) {
         // no locality op anywhere in the horizon: the whole tail is static
 #pragma unroll
@@ -873,7 +880,12 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                                     }
                                 }
                             } else {
+#ifdef FATE_AB
+                                const int L = (lay.diag & 8) ? (raw.z & 1) - 1 + (raw.z & 2)
+                                                             : loc_row[raw.z];
+#else
                                 const int L = loc_row[raw.z];
+#endif
                                 keep = L >= 0;
                                 if (!MASKW) {
                                     mlo = (unsigned)(OVR ? V6_KEY_SIGMA + L : L);
@@ -896,6 +908,12 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                         j0 += 32;
                     } while (j0 < t1 && base + 32 <= lay.ops_cap);
                     // walk the buffered chunk
+#ifdef FATE_AB
+                    if (lay.diag & 4) {
+                        __syncwarp();
+                        continue;
+                    }
+#endif
                     if (MASKW) {
                         // pad to a multiple of 4 with entries that match no device;
                         // walk 4 ops per iteration (two 16-byte mask loads, two
@@ -964,6 +982,12 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         }
     }
 
+#ifdef FATE_AB
+    if (lay.diag & 2) {
+        if (t == 0) out.psi[work.psi_off[item]] = tail[0] + bb;
+        return;
+    }
+#endif
     // ---- P4: per-device assembly ----------------------------------------------------------------
     // Shard bound R = 2 with every class tabulated:
     // a device's second shard always goes to the first idle device other than

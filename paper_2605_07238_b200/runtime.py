@@ -369,8 +369,10 @@ class DeviceWork:
         key = int(stream.cuda_stream)
         q = self._queues.get(key)
         if q is None:
-            q = self._queues[key] = self._torch.zeros(2, dtype=self._torch.int32,
-                                                      device=self._device)
+            # zero-filled on `stream` itself, so ordered before its first launch
+            with self._torch.cuda.stream(stream):
+                q = self._queues[key] = self._torch.zeros(2, dtype=self._torch.int32,
+                                                          device=self._device)
         return q.data_ptr()
 
 

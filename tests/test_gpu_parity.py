@@ -430,8 +430,16 @@ def test_more_concurrent_launches_than_rotating_counter_slots():
     n = case.work.n_psi
     dbank = runtime.DeviceBank(case.bank, case.weights)
     ds, dw = dbank.upload_states(case.states), dbank.upload_work(case.work)
+    from cuda.bindings import runtime as cudart
+
     outs = [dbank.alloc_out(case.work, extras=False) for _ in range(160)]
-    streams = [torch.cuda.Stream() for _ in outs]
+    # 160 distinct CUDA streams (torch's own stream pool recycles 32)
+    raw = []
+    for _ in outs:
+        err, h = cudart.cudaStreamCreateWithFlags(cudart.cudaStreamNonBlocking)
+        assert err == cudart.cudaError_t.cudaSuccess
+        raw.append(h)
+    streams = [torch.cuda.ExternalStream(int(h)) for h in raw]
     gate = torch.cuda.Event()
     hold = torch.cuda.current_stream()
     torch.cuda._sleep(20_000_000)  # keep the streams' launches queued together
@@ -443,3 +451,5 @@ def test_more_concurrent_launches_than_rotating_counter_slots():
     assert len(dw._queues) == 160
     for o in outs:
         assert np.array_equal(bits(o.psi.cpu().numpy()[:n]), want)
+    for h in raw:
+        cudart.cudaStreamDestroy(h)

@@ -21,9 +21,18 @@ def main():
     dev = torch.device("cuda:0")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     out = {"lib": os.environ.get("KB_TAG", "")}
+    order = os.environ.get("KB_C4_ORDER", "scenario")  # or "stage": v-major C4 items
     for name, build in (("c5", lambda: bench.build_c5(bench.shard_plan(0, 1), "frontier")),
                         ("c4", lambda: bench.build_c4("sweep"))):
         cfg, bank, states, work = build()
+        if name == "c4" and order == "stage":
+            import numpy as np
+
+            from paper_2605_07238_b200 import pack
+
+            idx = np.lexsort((work.scen, work.stage))
+            work = pack.make_work(bank, zip(work.scen[idx].tolist(), work.stage[idx].tolist()),
+                                  cfg.weights.ablation.no_shard)
         db = runtime.DeviceBank(bank, cfg.weights, device=dev)
         ds, dw = db.upload_states(states), db.upload_work(work)
         o = db.alloc_out(work, extras=True)

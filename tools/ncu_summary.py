@@ -54,6 +54,29 @@ def phases_of(src_path):
     return marks
 
 
+# Inlined helpers are reported at their own source lines; attribute them to
+# the kernel phase that calls them (the item phases are banner-delimited).
+HELPER_PHASE = {"v6_apply": "P3", "v6_apply_m": "P3", "v6_cached_tokens": "P0",
+                "v6_qc": "P2", "v6_qc_value": "P2", "v6_div1000": "P4", "v6_div": "P4"}
+
+
+def helpers_of(src_path):
+    """(first line, last line, phase) of each helper function of the kernel
+    source that HELPER_PHASE names."""
+    lines = open(src_path).read().split("\n")
+    starts = []
+    for i, line in enumerate(lines, 1):
+        m = re.match(r"\s*__device__.*?\b(v6_\w+)\s*\(", line)
+        if m:
+            starts.append((i, m.group(1)))
+    out = []
+    for k, (ln, name) in enumerate(starts):
+        end = starts[k + 1][0] - 1 if k + 1 < len(starts) else len(lines)
+        if name in HELPER_PHASE:
+            out.append((ln, end, HELPER_PHASE[name]))
+    return out
+
+
 def per_line(rep):
     text = ncu(rep, "--page", "source", "--csv", "--print-source", "cuda,sass")
     agg = defaultdict(lambda: [0.0, 0.0])
@@ -92,17 +115,24 @@ def main():
         return
     agg = per_line(rep)
     marks = phases_of(src)
+    helpers = helpers_of(src)
     base = os.path.basename(src)
     tot_s = sum(v[0] for v in agg.values()) or 1
     tot_i = sum(v[1] for v in agg.values()) or 1
     out = defaultdict(lambda: [0.0, 0.0])
     for (f, line), (s, i) in agg.items():
         name = "helpers:" + f
+        if f.startswith("sm_") and "intrinsics" in f:
+            name = "warp intrinsics (shfl/ballot/match)"
         if f == base:
             name = "prologue"
             for ln, ph in marks:
                 if line >= ln:
                     name = ph
+            for a, b, ph in helpers:
+                if a <= line <= b:
+                    name = ph
+                    break
         out[name][0] += s
         out[name][1] += i
     print(f"\nSASS instructions {tot_i:.4g}" + (f" ({tot_i / n_items:.0f} per item)" if n_items else ""))

@@ -2,7 +2,7 @@
 arm, launch list, ncu details, per-phase summaries) and refresh
 profiles/ncu_traffic.json (the bench's roofline.traffic source).
 
-    python tools/save_profiles.py gpurun_out/<dir> <tag>
+    python tools/save_profiles.py gpurun_out/<dir> <tag> [round prefix, default r02]
 """
 import json
 import os
@@ -17,22 +17,22 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KERNEL_SRC = os.path.join(ROOT, "paper_2605_07238_b200", "csrc", "fate_score_v6.cuh")
 
 
-def main(src, tag):
+def main(src, tag, rnd="r02"):
     prof = os.path.join(ROOT, "profiles")
     for name, dst in (("bench.json", "bench.json"), ("bench_ref.json", "reference_arm.json"),
                       ("launches_c5.csv", "launches_c5.csv")):
         if os.path.exists(os.path.join(src, name)):
-            shutil.copy(os.path.join(src, name), os.path.join(prof, f"r01_{tag}_{dst}"))
+            shutil.copy(os.path.join(src, name), os.path.join(prof, f"{rnd}_{tag}_{dst}"))
     traffic = {"_comment": f"dram__bytes_read.sum + dram__bytes_write.sum of one fate_score "
-                           f"launch (ncu --set full); kernel {tag} (profiles/r01_{tag}_*)"}
+                           f"launch (ncu --set full); kernel {tag} (profiles/{rnd}_{tag}_*)"}
     items = {"c5": 102400, "c4": 80000}
     for k, key in (("c5", "c5_frontier"), ("c4", "c4_sweep")):
         rep = os.path.join(src, f"{k}_full.ncu-rep")
         if not os.path.exists(rep):
             continue
-        with open(os.path.join(prof, f"r01_{tag}_{k}_details.csv"), "w") as fh:
+        with open(os.path.join(prof, f"{rnd}_{tag}_{k}_details.csv"), "w") as fh:
             subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], stdout=fh, check=True)
-        with open(os.path.join(prof, f"r01_{tag}_{k}_summary.txt"), "w") as fh:
+        with open(os.path.join(prof, f"{rnd}_{tag}_{k}_summary.txt"), "w") as fh:
             subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep,
                             KERNEL_SRC, str(items[k])], stdout=fh, check=True)
         m = ns.raw_metrics(rep)
@@ -56,4 +56,4 @@ def main(src, tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], *(sys.argv[3:4]))
