@@ -109,3 +109,33 @@ def test_c1_from_reference_instance_json(scorer):
     _, problems, n_psi = G.replay(r, arrs, inst, cfg, scorer)
     assert not problems, problems[:3]
     assert n_psi > 0
+
+
+def test_compat_install_gpu_scorer_in_unmodified_reference():
+    """compat.install() with the GPU scorer: the reference's own factory
+    (wfsched.harness.make_policy, as run_manifest calls it) returns the GPU
+    policy, and the reference executor reproduces the captured config-1 and
+    config-3 runs exactly."""
+    import wfsched.executor as RE
+    import wfsched.harness as RH
+
+    from paper_2605_07238_b200 import compat
+    from paper_2605_07238_b200.planner import FateGpuPolicy
+
+    bad = []
+    compat.install(scorer=GpuScorer())
+    try:
+        for name in ("c1", "c3"):
+            runs, _ = G.load(name)
+            for r in runs:
+                if name == "c1":
+                    inst, cfg = G.c1_setup(r["variant"])
+                else:
+                    inst, cfg = G.c3_setup(r["ratio"], r["batch"], r["shape"])
+                pol = RH.make_policy("fate")
+                assert isinstance(pol, FateGpuPolicy)
+                rec = RE.run(pol, inst, cfg)
+                bad += G.record_mismatches(rec, r["record"])[:2]
+    finally:
+        compat.uninstall()
+    assert not bad, bad

@@ -364,30 +364,27 @@ def test_captured_pipeline_invalidated_by_larger_batch():
     pipe.close()
 
 
-def test_c4_full_sweep_scenario_and_c5_full_frontier():
-    """Full-size parity: every stage of a config-4 scenario (10 000 stages x
-    64 devices x <= 2 slots, ~1.1 M Psi) and the full config-5 frontier of
-    512 instances (~0.7 M Psi), each bit-identical to the oracle."""
+def test_bench_batches_in_full():
+    """The bench's own batches, in full, bit-identical to the oracle: every
+    Psi, S and completion of the config-5 frontier batch (4096 instances,
+    5.72 M Psi, bench.build_c5) and every Psi of the config-4 sweep (all 8
+    scenario states x 10 000 stages, 9.0 M Psi, bench.build_c4)."""
     import bench
-    from paper_2605_07238_b200 import fastgen, scenarios
 
-    cfg, bank, states, work = bench.build_c4("sweep", n_scen=1, first_scen=2)
+    cfg, bank, states, work = bench.build_c5(bench.shard_plan(0, 1), "frontier")
+    want = oracle.score(bank, pack.weights_record(cfg.weights), states, work)
+    res = runtime.DeviceBank(bank, cfg.weights).score(states, work, extras=True)
+    assert work.n_psi == 5_722_208
+    for k in ("psi", "sched", "completion"):
+        got = getattr(res, k).cpu().numpy()[: want[k].size]
+        assert np.array_equal(bits(got), bits(want[k])), k
+
+    cfg, bank, states, work = bench.build_c4("sweep")
     want = oracle.score(bank, pack.weights_record(cfg.weights), states, work,
                         with_extras=False)["psi"]
-    dbank = runtime.DeviceBank(bank, cfg.weights)
-    got = dbank.score(states, work, extras=False).psi.cpu().numpy()[: work.n_psi]
-    assert work.n_psi > 1_000_000
-    assert np.array_equal(bits(got), bits(want))
-
-    cfg5 = scenarios.config_c5()
-    fb = fastgen.synth_batch(cfg5, 512, 1000, 0, 20, 25, 0.12, 16)
-    sc, g = fb.frontier_items()
-    work5 = pack.make_work(fb.bank, zip(sc.tolist(), g.tolist()), False)
-    want5 = oracle.score(fb.bank, pack.weights_record(cfg5.weights), fb.states, work5,
-                         with_extras=False)["psi"]
-    d5 = runtime.DeviceBank(fb.bank, cfg5.weights)
-    got5 = d5.score(fb.states, work5, extras=False).psi.cpu().numpy()[: work5.n_psi]
-    assert np.array_equal(bits(got5), bits(want5))
+    got = runtime.DeviceBank(bank, cfg.weights).score(states, work, extras=False).psi
+    assert work.n_psi == 9_003_008
+    assert np.array_equal(bits(got.cpu().numpy()[: work.n_psi]), bits(want))
 
 
 def test_prepare_rejects_false_bank_declarations_and_nonfinite_ops():

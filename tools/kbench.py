@@ -37,6 +37,8 @@ def main():
         ds, dw = db.upload_states(states), db.upload_work(work)
         o = db.alloc_out(work, extras=True)
         o.tail = None
+        if os.environ.get("KB_NO_SCHED"):
+            o.sched = None
         ms = []
         for _ in range(reps):
             m, _ = bench.time_device(torch, db, ds, dw, o, steps, 5, flush, 1, dev)
