@@ -686,8 +686,13 @@ def run_fate(args):
     from paper_2605_07238_b200 import pack, runtime
 
     rank, world, local = dist_env()
+    if args.share_device:  # plumbing check only: every rank on cuda:0 (gloo)
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(args.dist_backend)
     device = torch.device(f"cuda:{local}")
     torch.cuda.set_device(device)
     nvtx = torch.cuda.nvtx
@@ -809,16 +814,19 @@ def run_fate(args):
     c4 = None
     if args.workload == "c5" and not args.no_c4:
         c4 = measure_c4(torch, device, args, rank, world)
-    c2 = None
+    c2 = api = None
     if rank == 0 and world == 1 and args.workload == "c5" and not args.no_c2:
         nvtx.range_push("c2_fate_runs")
         c2 = measure_c2_runs()
+        api = measure_api_waves()
         nvtx.range_pop()
 
     items_total = reduce_sum(float(work.n_items), world, device)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            **({"validation_only": f"{world} ranks shared one GPU over {args.dist_backend}; "
+                                   "not a scaling measurement"} if args.share_device else {}),
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (config-5 generator + canonical scenario states, SURVEY §8(d))",
@@ -840,6 +848,8 @@ def run_fate(args):
             line["c4_sweep"] = c4
         if c2 is not None:
             line["c2_fate_runs"] = c2
+        if api is not None:
+            line["api_build_problem"] = api
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -913,6 +923,78 @@ def measure_c2_runs() -> dict | None:
     return out
 
 
+def measure_api_waves() -> dict | None:
+    """One planning wave through the drop-in API with the caller's objects:
+    ``planner.build_problem(frontier, state, cost_model, dag)`` (reference
+    ExecutionState in, reference FrontierProblem out: pack, H2D, kernel, D2H
+    and the Candidate tuples, wall clock) against the reference's own
+    ``build_problem`` on the same wave -- in full for a config-1 wave, on a
+    sample of candidates (then extrapolated) for a config-4 frontier wave,
+    where the reference takes ~0.1 s per candidate."""
+    reference_on_path()
+    try:
+        import wfsched.benchgen as RB
+        import wfsched.planner as RPl
+        from wfsched.config import default_config
+        from wfsched.costs import CostModel
+        from wfsched.model import ready_set
+        from wfsched.state import ExecutionState
+    except ImportError:
+        return None
+    from dataclasses import replace
+
+    from paper_2605_07238_b200 import planner, scenarios
+
+    def gpu_wave(front, st, cm, dag, reps=5):
+        scorer = planner.GpuScorer()
+        planner.build_problem(front, st, cm, dag, scorer=scorer)  # bank upload + prologue
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            prob = planner.build_problem(front, st, cm, dag, scorer=scorer)
+            ts.append(time.perf_counter() - t0)
+        return prob, sorted(ts)[len(ts) // 2]
+
+    out = {}
+    cfg = default_config(4)
+    cfg = cfg.with_weights(replace(cfg.weights, horizon=2))
+    inst = RB.lifted_instance("soykb", cfg, seed=11, batch_size=16, scale=1.0, min_groups=50)
+    cm = CostModel(cfg.models, cfg.topology, cfg.weights)
+    st = ExecutionState.initial(inst, cfg.topology.device_ids)
+    front = set(ready_set(inst.dag, st.completed))
+    prob, gpu_s = gpu_wave(front, st, cm, inst.dag)
+    t0 = time.perf_counter()
+    want = RPl.build_problem(front, st, cm, inst.dag)
+    ref_s = time.perf_counter() - t0
+    out["c1_first_wave"] = {"candidates": len(prob.candidates), "gpu_ms": 1e3 * gpu_s,
+                            "reference_ms": 1e3 * ref_s,
+                            "identical": prob.candidates == want.candidates}
+
+    cfg4 = scenarios.config_c4_catalog()
+    dag = RB.synth_generate(RB.SuiteSpec(kind="synthetic", depth=100, width=100, density=0.03,
+                                         seed=1, batch_size=16), cfg4)
+    inst4 = RB.make_instance(dag, 16, 1)
+    st4 = scenarios.build_scenario(inst4, cfg4, 0)
+    cm4 = CostModel(cfg4.models, cfg4.topology, cfg4.weights)
+    front4 = set(ready_set(inst4.dag, st4.completed))
+    prob4, gpu4 = gpu_wave(front4, st4, cm4, inst4.dag)
+    sample = prob4.candidates[:16]
+    t0 = time.perf_counter()
+    ref = [cm4.plan_score(inst4.dag.stages[c.stage_id], c.slot, c.device_id, st4, inst4.dag)
+           for c in sample]
+    ref_s = time.perf_counter() - t0
+    rate = len(sample) / ref_s
+    out["c4_frontier_wave"] = {
+        "candidates": len(prob4.candidates), "gpu_ms": 1e3 * gpu4,
+        "reference_candidates_per_s": rate,
+        "reference_s_extrapolated": len(prob4.candidates) / rate,
+        "sample_identical": [c.psi.hex() for c in sample] == [x.hex() for x in ref],
+        "sample": f"first {len(sample)} candidates with CostModel.plan_score (1 core)"}
+    out["path"] = ("planner.build_problem: wfsched ExecutionState -> pack_states -> H2D -> "
+                   "fate_score -> D2H -> wfsched.planner.FrontierProblem (wall clock, median of 5)")
+    return out
+
+
 def measure_c4(torch, device, args, rank: int = 0, world: int = 1) -> dict:
     from paper_2605_07238_b200 import pack, runtime
 
@@ -951,6 +1033,10 @@ def main(argv=None):
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-weak", action="store_true")
     ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
+    ap.add_argument("--share-device", action="store_true",
+                    help="every rank on cuda:0 (with --dist-backend gloo): validates the "
+                         "multi-rank plan on one GPU; its timings are not scaling numbers")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-instances", type=int, default=8)
     ap.add_argument("--ref-pool", type=int, default=32)
