@@ -418,6 +418,49 @@ def pack_states(bank: PackedBank, scenarios, kappa_cap: int | None = None) -> Pa
     return PackedStates(arrays=arrays, n_scenarios=n_s, kappa_cap=cap)
 
 
+def pack_state_into(bank: PackedBank, inst: int, st, v: dict, cap: int) -> None:
+    """:func:`pack_states` for one scenario ``(inst, st)``, written into
+    preallocated arrays ``v`` (the fate_state fields; ``loc`` sized to the
+    instance, ``kappa`` to ``n_devices * cap * 4``) -- the per-wave form used
+    by :class:`~.runtime.WaveRunner`'s pinned staging block."""
+    n_dev = bank.scalars["n_devices"]
+    v["scen_inst"][0] = inst
+    v["scen_clock"][0] = float(st.clock)
+    v["scen_loc_off"][0] = 0
+    row = v["loc"]
+    row.fill(-1)
+    dev_index, sindex = bank.dev_index, bank.stage_index[inst]
+    g0 = int(bank.inst_stage_off[inst])
+    lvl = bank.arrays["st_level"]
+    done = -1
+    for sid in st.parent_loc:
+        dev = st.output_device(sid)
+        i = sindex.get(sid)
+        if dev is not None and i is not None:
+            row[i] = dev_index[dev]
+            lv = int(lvl[g0 + i])
+            if lv > done:
+                done = lv
+    v["scen_done_level"][0] = done
+    res, free, kn = v["residency"], v["dev_free"], v["kappa_n"]
+    kap = v["kappa"][: n_dev * cap * 4].reshape(n_dev, cap, 4)
+    kap.fill(0)
+    res.fill(-1)
+    free.fill(0.0)
+    kn.fill(0)
+    for dev, di in dev_index.items():
+        res[di] = bank.model_id(st.residency.get(dev))
+        free[di] = float(st.device_free.get(dev, 0.0))
+        ents = st.prefix_store.get(dev, {})
+        if len(ents) > cap:
+            raise ValueError(f"{len(ents)} prefix entries on {dev} exceed capacity {cap}")
+        kn[di] = len(ents)
+        for k, ent in enumerate(ents.values()):
+            kap[di, k, 0] = bank.group_id(ent.group)
+            kap[di, k, 1] = int(ent.tokens)
+            kap[di, k, 2] = bank.model_id(ent.model)
+
+
 # ---------------------------------------------------------------------------
 # work lists
 # ---------------------------------------------------------------------------

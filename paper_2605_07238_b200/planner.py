@@ -37,7 +37,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import pack
-from .runtime import DeviceBank
+from .runtime import DeviceBank, WaveRunner, WaveStaging
 
 
 def _wf(name: str):
@@ -93,32 +93,47 @@ class GpuScorer:
         self.max_banks = max_banks
         self.device = device
         self.kernel_seconds = 0.0
+        self.bank_seconds = 0.0  # packing + uploading banks (once per instance)
+        self._staging = None
 
-    def bank_for(self, instance, models, topo, weights) -> DeviceBank:
+    def _entry(self, instance, models, topo, weights):
         key = (id(instance), id(models), id(topo), weights)
         hit = self._banks.get(key)
         if hit is not None and hit[0] is instance:
             self._banks.move_to_end(key)
-            return hit[1]
+            return hit
+        t0 = time.perf_counter()
         packed = pack.pack_bank([instance], models, topo)
         dbank = DeviceBank(packed, weights, device=self.device)
-        self._banks[key] = (instance, dbank, models, topo)  # strong refs: no id() reuse
+        self.bank_seconds += time.perf_counter() - t0
+        hit = [instance, dbank, models, topo, None]  # strong refs: no id() reuse
+        self._banks[key] = hit
         while len(self._banks) > self.max_banks:
             self._banks.popitem(last=False)
-        return dbank
+        return hit
+
+    def bank_for(self, instance, models, topo, weights) -> DeviceBank:
+        return self._entry(instance, models, topo, weights)[1]
 
     def score_wave(self, frontier, state, cost_model, dag=None) -> WaveScores:
+        """One launch per wave through the bank's :class:`~.runtime.WaveRunner`
+        (one H2D, one kernel, one D2H)."""
         instance = state.instance
         if dag is not None and dag is not instance.dag and dag != instance.dag:
             raise ValueError("dag must be the state's instance dag")
-        dbank = self.bank_for(instance, cost_model.models, cost_model.topo, cost_model.weights)
-        packed = dbank.packed
+        entry = self._entry(instance, cost_model.models, cost_model.topo, cost_model.weights)
+        dbank, runner = entry[1], entry[4]
+        if runner is None:
+            if self._staging is None:
+                self._staging = WaveStaging(dbank.torch, dbank.device)
+            runner = entry[4] = WaveRunner(dbank, self._staging)
         sids = sorted(frontier)
-        states = pack.pack_states(packed, [(0, state)])
-        work = pack.make_work(packed, [(0, packed.global_index(0, s)) for s in sids],
-                              dbank.no_shard)
-        res = dbank.score(states, work, extras=True, timing=True)
-        return wave_scores(packed, sids, work, res)
+        r = runner.run(state, sids)
+        el = runner.elig[r["stage"] - runner.g0]
+        return WaveScores(stage_ids=sids, bounds=r["bounds"].tolist(),
+                          device_ids=dbank.packed.device_ids, elig=el.tolist(), psi=r["psi"],
+                          psi_off=r["psi_off"], sched=r["sched"],
+                          completion=r["completion"], tail=r["tail"], timing=r["timing"])
 
 
 def wave_scores(packed, sids, work, res) -> WaveScores:

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import abi
-from .pack import PackedBank, PackedStates, WorkList, weights_record
+from .pack import PackedBank, PackedStates, WorkList, pack_state_into, weights_record
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfate.so")
@@ -478,3 +478,136 @@ class HostPipeline:
             self.close()
         except Exception:
             pass
+
+
+class WaveStaging:
+    """Grow-only staging shared by the :class:`WaveRunner` of every bank of a
+    scorer (waves are scored one at a time): one pinned host input block and
+    one device input block (``fate_state`` + ``fate_work`` SoA at offsets set
+    per wave), one device output block and its pinned host mirror, and the
+    ticket counter of the work list (self-resetting, fate_work.queue).
+    Pinned allocations are slow, so blocks are reused and only regrown (x2)."""
+
+    def __init__(self, torch, device):
+        self.torch = torch
+        self.device = device
+        self.in_bytes = 0
+        self.out_len = 0
+        self.queue = torch.zeros(2, dtype=torch.int32, device=device)
+
+    def ensure(self, in_bytes: int, out_len: int) -> None:
+        torch = self.torch
+        if in_bytes > self.in_bytes or out_len > self.out_len:
+            torch.cuda.current_stream(self.device).synchronize()
+        if in_bytes > self.in_bytes:
+            self.in_bytes = max(in_bytes, 2 * self.in_bytes, 4096)
+            self.h_in = torch.empty(self.in_bytes, dtype=torch.uint8, pin_memory=True)
+            self.h_in_np = self.h_in.numpy()
+            self.d_in = torch.empty(self.in_bytes, dtype=torch.uint8, device=self.device)
+        if out_len > self.out_len:
+            self.out_len = max(out_len, 2 * self.out_len, 4096)
+            self.h_out = torch.empty(self.out_len, dtype=torch.float64, pin_memory=True)
+            self.h_out_np = self.h_out.numpy()
+            self.d_out = torch.empty(self.out_len, dtype=torch.float64, device=self.device)
+
+
+class WaveRunner:
+    """One scenario of one bank instance, scored per wave with the fewest
+    host<->device round trips (the drop-in's hot loop: ``build_problem`` is
+    called once per executor wave, reference ``policies.py:62``).
+
+    Per wave: the snapshot is written straight into the pinned staging block
+    (``pack.pack_state_into``, the single-scenario form of
+    ``pack.pack_states``) with the work list, then one H2D copy, one
+    ``fate_score`` launch, one D2H copy of Psi | S | completion | tail |
+    timing and one stream synchronize."""
+
+    _IN = (("scen_inst", np.int32, "1"), ("scen_clock", np.float64, "1"),
+           ("scen_loc_off", np.int64, "1"), ("scen_done_level", np.int32, "1"),
+           ("residency", np.int32, "D"), ("dev_free", np.float64, "D"),
+           ("kappa_n", np.int32, "D"), ("kappa", np.int32, "K"), ("loc", np.int32, "N"),
+           ("scen", np.int32, "W"), ("stage", np.int32, "W"), ("psi_off", np.int64, "W"))
+
+    def __init__(self, dbank: DeviceBank, staging: WaveStaging, inst: int = 0):
+        p = dbank.packed
+        self.dbank = dbank
+        self.staging = staging
+        self.L = load_library()
+        self.inst = inst
+        self.D = p.scalars["n_devices"]
+        self.g0 = int(p.inst_stage_off[inst])
+        self.n_local = len(p.stage_ids[inst])
+        self.sindex = p.stage_index[inst]
+        g = np.arange(self.g0, self.g0 + self.n_local)
+        if dbank.no_shard:
+            self.bounds = np.ones(self.n_local, dtype=np.int32)
+        else:
+            from .pack import popcount64
+
+            self.bounds = np.minimum(p.arrays["st_shard"][g],
+                                     popcount64(p.arrays["st_elig"][g])).astype(np.int32)
+        self.elig = p.arrays["st_elig"][g]
+        self.cap = 1
+
+    def _layout(self, cap: int, n_items: int) -> tuple:
+        sizes = {"1": 1, "D": self.D, "K": self.D * cap * 4, "N": max(self.n_local, 1),
+                 "W": max(n_items, 1)}
+        off, offs = 0, {}
+        for name, dt, n in self._IN:
+            offs[name] = (off, dt, sizes[n])
+            off += (sizes[n] * np.dtype(dt).itemsize + 15) & ~15
+        return offs, off
+
+    def run(self, st, sids) -> dict:
+        """Score the frontier ``sids`` (sorted stage ids) of snapshot ``st``;
+        returns host copies: psi (slot-major rows per stage), psi_off, bounds,
+        stage (global), sched / completion / tail [n, D], timing [n, D, 3]."""
+        stg = self.staging
+        torch = stg.torch
+        D = self.D
+        need = max((len(e) for e in st.prefix_store.values()), default=0)
+        if need > 64:
+            raise ValueError(f"{need} prefix entries per device exceed 64")
+        cap = max(self.cap, need)
+        self.cap = cap
+        n = len(sids)
+        loc = np.fromiter((self.sindex[s] for s in sids), dtype=np.int64, count=n)
+        bounds = self.bounds[loc]
+        off = np.zeros(n, dtype=np.int64)
+        if n:
+            np.cumsum(bounds[:-1].astype(np.int64) * D, out=off[1:])
+        n_psi = int(bounds.astype(np.int64).sum()) * D
+        nd = n * D
+        total = n_psi + 6 * nd
+        offs, in_bytes = self._layout(cap, n)
+        stg.ensure(in_bytes, total)
+        buf = stg.h_in_np
+        v = {k: buf[o: o + m * np.dtype(dt).itemsize].view(dt) for k, (o, dt, m) in offs.items()}
+        pack_state_into(self.dbank.packed, self.inst, st, v, cap)
+        v["scen"][:n] = 0
+        v["stage"][:n] = loc + self.g0
+        v["psi_off"][:n] = off
+        base = stg.d_in.data_ptr()
+        cstate = abi.FateState(n_scenarios=1, kappa_cap=cap)
+        for k in abi.STATE_PTRS:
+            setattr(cstate, k, base + offs[k][0])
+        cwork = abi.FateWork(n_items=n, scen=base + offs["scen"][0],
+                             stage=base + offs["stage"][0], psi_off=base + offs["psi_off"][0],
+                             queue=stg.queue.data_ptr())
+        o_s, o_c, o_t, o_m = n_psi, n_psi + nd, n_psi + 2 * nd, n_psi + 3 * nd
+        ob = stg.d_out.data_ptr()
+        cout = abi.FateOut(psi=ob, sched=ob + 8 * o_s, completion=ob + 8 * o_c,
+                           tail=ob + 8 * o_t, timing=ob + 8 * o_m)
+        s = torch.cuda.current_stream(self.dbank.device)
+        d = self.dbank
+        stg.d_in[:in_bytes].copy_(stg.h_in[:in_bytes], non_blocking=True)
+        if n:
+            _check(self.L.fate_score(C.byref(d.cbank), C.byref(d.cweights), C.byref(d.cwin),
+                                     C.byref(d.cder), C.byref(cstate), C.byref(cwork),
+                                     C.byref(cout), C.c_void_p(s.cuda_stream)), "fate_score")
+            stg.h_out[:total].copy_(stg.d_out[:total], non_blocking=True)
+        s.synchronize()
+        h = stg.h_out_np[:total].copy()
+        return {"psi": h[:n_psi], "psi_off": off, "bounds": bounds, "stage": loc + self.g0,
+                "sched": h[o_s:o_c].reshape(n, D), "completion": h[o_c:o_t].reshape(n, D),
+                "tail": h[o_t:o_m].reshape(n, D), "timing": h[o_m:total].reshape(n, D, 3)}

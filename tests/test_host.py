@@ -293,3 +293,54 @@ def test_production_library_has_one_kernel_generation():
     for knob in (b"FATE_SCORE_KERNEL", b"FATE_MINB", b"FATE_V6_OPCAP", b"FATE_V6_FETCH",
                  b"FATE_PIPE_TRACE", b"FATE_V6_DYNLAYOUT"):
         assert knob not in blob, knob
+
+
+def _capture_waves(inst, cfg):
+    """(frontier, snapshot state, cost model) of every wave of one reference
+    FATE run (the reference's own build_problem, wrapped)."""
+    import wfsched.executor as RE
+    import wfsched.policies as RP
+
+    seen = []
+    real = RP.build_problem
+
+    def spy(frontier, state, cost_model, dag):
+        seen.append((set(frontier), state, cost_model))
+        return real(frontier, state, cost_model, dag)
+
+    RP.build_problem = spy
+    try:
+        RE.run(RP.make_policy("fate"), inst, cfg)
+    finally:
+        RP.build_problem = real
+    return seen
+
+
+@pytest.mark.parametrize("which", ["c1", "c3"])
+def test_wave_packer_equals_pack_states(which):
+    """WaveRunner's single-scenario packer (pack.pack_state_into, written into
+    the pinned staging block) gives the same fate_state arrays as
+    pack.pack_states on every wave of a reference run."""
+    import golden_replay as GR
+
+    inst, cfg = GR.c1_setup({}) if which == "c1" else GR.c3_setup(0.5, 16, 1)
+    waves = _capture_waves(inst, cfg)
+    assert waves
+    bank = pack.pack_bank([inst], cfg.models, cfg.topology)
+    D = bank.scalars["n_devices"]
+    n = len(bank.stage_ids[0])
+    for frontier, st, _ in waves:
+        ref = pack.pack_states(bank, [(0, st)])
+        cap = ref.kappa_cap + 2
+        v = {"scen_inst": np.zeros(1, np.int32), "scen_clock": np.zeros(1), "scen_loc_off":
+             np.zeros(1, np.int64), "scen_done_level": np.zeros(1, np.int32),
+             "residency": np.zeros(D, np.int32), "dev_free": np.zeros(D),
+             "kappa_n": np.zeros(D, np.int32), "kappa": np.zeros(D * cap * 4, np.int32),
+             "loc": np.zeros(n, np.int32)}
+        pack.pack_state_into(bank, 0, st, v, cap)
+        for k in ("scen_inst", "scen_clock", "scen_loc_off", "scen_done_level", "residency",
+                  "dev_free", "kappa_n", "loc"):
+            assert np.array_equal(v[k], ref.arrays[k]), k
+        got = v["kappa"].reshape(D, cap, 4)[:, : ref.kappa_cap]
+        assert np.array_equal(got, ref.arrays["kappa"].reshape(D, ref.kappa_cap, 4))
+        assert not v["kappa"].reshape(D, cap, 4)[:, ref.kappa_cap:].any()

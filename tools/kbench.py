@@ -19,7 +19,9 @@ def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 30
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     dev = torch.device("cuda:0")
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    # KB_NOFLUSH=1: no L2 flush between steps (warm-L2 upper bound, diagnostics only)
+    nf = os.environ.get("KB_NOFLUSH")
+    flush = torch.empty(16 if nf else 64 * 1024 * 1024, dtype=torch.float32, device=dev)
     out = {"lib": os.environ.get("KB_TAG", "")}
     order = os.environ.get("KB_C4_ORDER", "scenario")  # or "stage": v-major C4 items
     for name, build in (("c5", lambda: bench.build_c5(bench.shard_plan(0, 1), "frontier")),
