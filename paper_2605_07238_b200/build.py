@@ -79,6 +79,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     # experiment-only preprocessor defines (A/B of kernel variants), e.g.
     # FATE_BUILD_DEFS="FATE_V6_NOPF"
     extra += ["-D" + d for d in os.environ.get("FATE_BUILD_DEFS", "").split()]
+    extra += os.environ.get("FATE_BUILD_NVCC", "").split()  # experiment-only nvcc flags
     cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-shared", "-Xptxas", "-v", *SOURCES, "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

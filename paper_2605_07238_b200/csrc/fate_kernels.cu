@@ -245,7 +245,7 @@ int ab_env(const char* name, int dflt, int lo, int hi) {
 }
 #endif
 
-template <int DPL, bool OVR, bool SL, int MINB, bool QG>
+template <int DPL, bool OVR, bool SL, int MINB, bool QG, bool UNIT = false>
 int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                  const fate_derived* der, const fate_state* st, const fate_work* work,
                  const fate_out* out, cudaStream_t s) {
@@ -269,7 +269,7 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     const size_t smem = (size_t)lay.item_bytes * 4;
     if (smem > 220 * 1024) return fail(FATE_ETOOBIG, "v6 shared-memory footprint too large");
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fate_score_v6_kernel<DPL, OVR, SL, MINB, QG>,
+        cudaFuncSetAttribute(fate_score_v6_kernel<DPL, OVR, SL, MINB, QG, UNIT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // persistent grid: every resident CTA slot once (capped by the item count)
     static thread_local size_t occ_smem = ~size_t(0);
@@ -277,11 +277,11 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     static thread_local const void* occ_fn = nullptr;
     int dev = 0;
     cudaGetDevice(&dev);
-    const void* fn = (const void*)fate_score_v6_kernel<DPL, OVR, SL, MINB, QG>;
+    const void* fn = (const void*)fate_score_v6_kernel<DPL, OVR, SL, MINB, QG, UNIT>;
     if (occ_smem != smem || occ_dev != dev || occ_fn != fn) {
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fate_score_v6_kernel<DPL, OVR, SL, MINB, QG>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fate_score_v6_kernel<DPL, OVR, SL, MINB, QG, UNIT>,
                                                       128, smem);
         o = std::max(1, sms * std::max(1, per));
         occ_smem = smem;
@@ -304,7 +304,7 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
     static std::atomic<int> slot{0};
     const int qs = g_queue_slot_override >= 0 ? g_queue_slot_override
                                               : slot.fetch_add(1) % V6_QDIRECT;
-    fate_score_v6_kernel<DPL, OVR, SL, MINB, QG><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
+    fate_score_v6_kernel<DPL, OVR, SL, MINB, QG, UNIT><<<blocks, 128, smem, s>>>(*bank, *w, *win, *der, *st,
                                                                     *work, *out, lay, qs, fetch);
     return 0;
 }
@@ -337,6 +337,15 @@ int launch_v5(const fate_bank* bank, const fate_weights* w, const fate_windows* 
 }
 #endif
 
+// The UNIT instantiation's precondition (fate_score_v6.cuh v6_item): no
+// ablation and every multiplicative identity weight exactly 1.0.
+inline bool v6_unit_weights(const fate_weights* w) {
+    return w->ablation == 0 && w->lambda_q == 1.0 && w->lambda_s == 1.0 &&
+           w->lambda_tr == 1.0 && w->state_scale == 1.0 && w->locality_scale == 1.0 &&
+           w->prefix_scale == 1.0 && w->transfer_x == 1.0 && w->prefix_x == 1.0 &&
+           w->kappa_prefix == 1.0;
+}
+
 // Lean instantiation (QG = false) when the bank declares that no query has a
 // prefix group (FATE_BANK_NO_QGROUPS) and every device has the same speed
 // (FATE_BANK_UNIFORM_SPEED) -- both verified by fate_prepare -- and the
@@ -349,8 +358,14 @@ int launch_v6_q(const fate_bank* bank, const fate_weights* w, const fate_windows
                 const fate_out* out, cudaStream_t s) {
     if (bank->has_overrides != 0)
         return launch_v6_mb<DPL, true, SL, MINB, true>(bank, w, win, der, st, work, out, s);
-    if ((bank->flags & FATE_BANK_NO_QGROUPS) && (bank->flags & FATE_BANK_UNIFORM_SPEED))
+    if ((bank->flags & FATE_BANK_NO_QGROUPS) && (bank->flags & FATE_BANK_UNIFORM_SPEED)) {
+#ifndef FATE_V6_NOUNIT
+        if (v6_unit_weights(w))
+            return launch_v6_mb<DPL, false, SL, MINB, false, true>(bank, w, win, der, st, work,
+                                                                   out, s);
+#endif
         return launch_v6_mb<DPL, false, SL, MINB, false>(bank, w, win, der, st, work, out, s);
+    }
     return launch_v6_mb<DPL, false, SL, MINB, true>(bank, w, win, der, st, work, out, s);
 }
 

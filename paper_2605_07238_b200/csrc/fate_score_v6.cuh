@@ -458,7 +458,13 @@ __device__ __forceinline__ double v6_qc(const fate_bank& b, const fate_state& st
 
 // One item (scenario, stage v) by one warp; sb = the warp's shared-memory slice
 // (static layout V6Static<DPL>::T when SL, else the runtime layout `lay`).
-template <int DPL, bool OVR, bool SL, bool QG>
+// UNIT: the weights' multiplicative identities are compile-time constants --
+// no ablation, and lambda_q = lambda_s = lambda_tr = state_scale =
+// locality_scale = prefix_scale = transfer_x = prefix_x = kappa_prefix = 1.0
+// (checked on the host, v6_unit_weights).  x * 1.0 == x and (-1.0) * x == -x
+// bit for bit (signed zeros included), so dropping those products is exact;
+// the kernel then carries no ablation branches or selects.
+template <int DPL, bool OVR, bool SL, bool QG, bool UNIT>
 __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& w,
                                         const fate_windows& win, const fate_derived& der,
                                         const fate_state& st, const fate_work& work,
@@ -484,8 +490,13 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     const unsigned FULL = 0xffffffffu;
     const int D = b.n_devices, LV = win.levels;
     const int Bmax = SL ? V6Static<DPL>::B : b.max_queries;  // row stride of s_rows
-    const bool no_loc = w.ablation & FATE_NO_LOCALITY;
-    const bool no_shard = w.ablation & FATE_NO_SHARD;
+    const bool no_loc = !UNIT && (w.ablation & FATE_NO_LOCALITY);
+    const bool no_shard = !UNIT && (w.ablation & FATE_NO_SHARD);
+    const double lam_q = UNIT ? 1.0 : w.lambda_q, lam_s = UNIT ? 1.0 : w.lambda_s;
+    const double lam_tr = UNIT ? 1.0 : w.lambda_tr, st_sc = UNIT ? 1.0 : w.state_scale;
+    const double loc_sc = UNIT ? 1.0 : w.locality_scale, pre_sc = UNIT ? 1.0 : w.prefix_scale;
+    const double tr_x = UNIT ? 1.0 : w.transfer_x, pre_x = UNIT ? 1.0 : w.prefix_x;
+    const double kap_p = UNIT ? 1.0 : w.kappa_prefix;
     const int H = w.eff_horizon;
     const int M1 = b.n_models + 1;
 
@@ -624,7 +635,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     }
 #pragma unroll
     for (int j = 0; j < DPL; ++j)
-        if (live[j]) s_tr[dv[j]] = trv[j] * w.transfer_x;
+        if (live[j]) s_tr[dv[j]] = trv[j] * tr_x;
     unsigned long long idle_m = 0ull, ok_m = 0ull;
 #pragma unroll
     for (int j = 0; j < DPL; ++j) {
@@ -965,10 +976,10 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                                 } else if (k < V6_KEY_SIGMA) {
                                     if (k - V6_KEY_MODEL == dmc[j]) aff[j] += val;
                                 } else if (k - V6_KEY_SIGMA != dv[j]) {
-                                    aff[j] -= w.lambda_tr *
+                                    aff[j] -= lam_tr *
                                               b.beta[(size_t)(k - V6_KEY_SIGMA) * D +
                                                      (live[j] ? dv[j] : 0)] *
-                                              val * w.transfer_x * w.locality_scale;
+                                              val * tr_x * loc_sc;
                                 }
                             }
                         }
@@ -1024,7 +1035,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     }
     double* psi = out.psi + work.psi_off[item];
     const double split = no_loc ? 0.0 : (bound > 1 ? c2.y : 0.0);
-    const bool no_pre = w.ablation & FATE_NO_PREFIX;
+    const bool no_pre = !UNIT && (w.ablation & FATE_NO_PREFIX);
     // One copy of the assembly code for both device slots (the loop is not
     // unrolled; slot values are selected, not indexed): halves this phase's
     // SASS for D > 32, which is instruction-cache bound.
@@ -1080,7 +1091,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             }
         }
         const double prefix =
-            w.kappa_prefix * (tokens == 0 ? 0.0 : v6_div1000(tokens)) * w.prefix_x;
+            kap_p * (tokens == 0 ? 0.0 : v6_div1000(tokens)) * pre_x;
 
         // _parallel_benefit (costs.py:181-201)
         const double full_total = sw + tr + here_j;
@@ -1135,10 +1146,10 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         const double colo_s = no_loc ? 0.0 : colo;
         const double prefix_s = no_pre ? 0.0 : prefix;
         const double par_s = no_shard ? 0.0 : parallel;
-        const double S = -w.lambda_q * wait - w.lambda_s * sw * w.state_scale
-                         - w.lambda_tr * tr_s * w.locality_scale
-                         + w.lambda_c * colo_s * w.locality_scale
-                         + w.lambda_p * prefix_s * w.prefix_scale + w.lambda_r * par_s;
+        const double S = -lam_q * wait - lam_s * sw * st_sc
+                         - lam_tr * tr_s * loc_sc
+                         + w.lambda_c * colo_s * loc_sc
+                         + w.lambda_p * prefix_s * pre_sc + w.lambda_r * par_s;
 
         if (out.sched) out.sched[orow] = S;
         if (out.tail) out.tail[orow] = tail_j;
@@ -1162,8 +1173,8 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
                 const double q2 = k == 1 ? hv * 0.5 : v6_div(hv, (double)(k + 1));
                 const double reduction = q1 - q2;
                 psi[(long long)k * D + d] = w.lambda_r * (reduction - overhead) -
-                                            w.lambda_q * wait - w.lambda_s * sw * w.state_scale -
-                                            w.lambda_tr * (tr_m + split) * w.locality_scale;
+                                            lam_q * wait - lam_s * sw * st_sc -
+                                            lam_tr * (tr_m + split) * loc_sc;
             }
         }
     }
@@ -1188,7 +1199,7 @@ constexpr int V6_QSLOTS = 256;
 constexpr int V6_QDIRECT = 128;
 __device__ unsigned int g_v6_queue[2 * V6_QSLOTS];  // per slot: next ticket, warps done
 
-template <int DPL, bool OVR, bool SL, int MINB, bool QG>
+template <int DPL, bool OVR, bool SL, int MINB, bool QG, bool UNIT>
 __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, fate_weights w,
                                                                   fate_windows win,
                                                                   fate_derived der, fate_state st,
@@ -1221,7 +1232,7 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
         const long long i1 = (long long)i + take < n ? (long long)i + take : n;
 #pragma unroll 1
         for (long long it = i; it < i1; ++it) {
-            v6_item<DPL, OVR, SL, QG>(b, w, win, der, st, work, out, lay, it, sb);
+            v6_item<DPL, OVR, SL, QG, UNIT>(b, w, win, der, st, work, out, lay, it, sb);
             __syncwarp();  // the slice is reused by the next item
         }
     }
