@@ -193,9 +193,11 @@ typedef struct fate_derived {
     double* tail_sum;               /* [n_stages*(n_models+1)] full tail value per
                                        (stage, displacement class) when no level has a
                                        locality op (costs.py:281-352) */
-    double* tail_static;            /* [n_stages*levels*(n_models+1)] affinity chain per
-                                       (stage, level, displacement class) with no locality
-                                       op applied (costs.py:307-331) */
+    double* tail_static;            /* [n_stages*levels*(n_models+1)] per (stage, level,
+                                       displacement class): the level's tail term
+                                       gamma**l * (affinity/len(bucket) + demand_coeff *
+                                       demand) with no locality op applied
+                                       (costs.py:307-351); 0 for an empty bucket */
     void* stage_rec;                /* [n_stages] 112-byte stage records (static per-stage
                                        scalars of one item, csrc/fate_score_v6.cuh V6Stage) */
     int64_t* tmpl_ptr;              /* [n_stages*levels+1] op-template offsets: exclusive

@@ -338,7 +338,8 @@ int launch_v5(const fate_bank* bank, const fate_weights* w, const fate_windows* 
 #endif
 
 // The UNIT instantiation's precondition (fate_score_v6.cuh v6_item): no
-// ablation and every multiplicative identity weight exactly 1.0.
+// ablation and every multiplicative identity weight exactly 1.0 (and, checked
+// at the call, D == 64 for two device slots).
 inline bool v6_unit_weights(const fate_weights* w) {
     return w->ablation == 0 && w->lambda_q == 1.0 && w->lambda_s == 1.0 &&
            w->lambda_tr == 1.0 && w->state_scale == 1.0 && w->locality_scale == 1.0 &&
@@ -360,7 +361,7 @@ int launch_v6_q(const fate_bank* bank, const fate_weights* w, const fate_windows
         return launch_v6_mb<DPL, true, SL, MINB, true>(bank, w, win, der, st, work, out, s);
     if ((bank->flags & FATE_BANK_NO_QGROUPS) && (bank->flags & FATE_BANK_UNIFORM_SPEED)) {
 #ifndef FATE_V6_NOUNIT
-        if (v6_unit_weights(w))
+        if (v6_unit_weights(w) && (DPL == 1 || bank->n_devices == 64))
             return launch_v6_mb<DPL, false, SL, MINB, false, true>(bank, w, win, der, st, work,
                                                                    out, s);
 #endif
@@ -694,7 +695,7 @@ int prepare(const fate_bank* bank, const fate_weights* w, const fate_windows* wi
             if (out->tail_static) {
                 const long long nt = n * (bank->n_models + 1);
                 fate_prepare_tail_static_kernel<<<(unsigned)((nt + threads - 1) / threads), threads, 0,
-                                                  s>>>(*bank, *w, *win, out->tail_static);
+                                                  s>>>(*bank, *w, *win, *out, out->tail_static);
                 g_launches++;
                 if ((rc = cuda_status("fate_prepare_tail_static_kernel"))) return rc;
                 if (out->tail_sum) {

@@ -10,11 +10,15 @@
 // whole horizon) without located window parents.
 
 
-// Prologue: static tail chains (no locality op applied) per (stage, level,
-// displacement class): class 0 = not displacing, class 1+m = displaces with
-// resident model m (costs.py:307-331).
+// Prologue: static tail level terms (no locality op applied) per (stage,
+// level, displacement class): class 0 = not displacing, class 1+m = displaces
+// with resident model m.  The affinity chain (costs.py:307-331) is folded
+// into the level's term gamma**l * (affinity/len(bucket) + demand_coeff *
+// demand) (costs.py:349-351) with the reference's operations, so a scoring
+// launch adds the stored term for a level without located window parents
+// (bit-identical to computing it there); 0 for an empty bucket.
 __global__ void fate_prepare_tail_static_kernel(fate_bank b, fate_weights w, fate_windows win,
-                                                double* tail_static) {
+                                                fate_derived der, double* tail_static) {
     const int M1 = b.n_models + 1;
     const int LV = win.levels;
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -45,7 +49,10 @@ __global__ void fate_prepare_tail_static_kernel(fate_bank b, fate_weights w, fat
                    w.prefix_scale;
         }
     }
-    tail_static[t] = aff;
+    const long long n = win.ptr[vl + 1] - win.ptr[vl];
+    const int l = (int)(vl - (long long)v * LV);
+    tail_static[t] =
+        n > 0 ? w.gamma_pow[l + 1] * (aff / (double)n + w.demand_coeff * der.demand[vl]) : 0.0;
 }
 
 // Prologue: full tail per (stage, displacement class) from the static level
@@ -64,8 +71,7 @@ __global__ void fate_prepare_tail_sum_kernel(fate_bank b, fate_weights w, fate_w
         const long long vl = v * LV + l;
         const long long n = win.ptr[vl + 1] - win.ptr[vl];
         if (n == 0) continue;
-        const double aff = der.tail_static[vl * M1 + c];
-        total += w.gamma_pow[l + 1] * (aff / (double)n + w.demand_coeff * der.demand[vl]);
+        total += der.tail_static[vl * M1 + c];  // the level's term
     }
     der.tail_sum[t] = total;
 }

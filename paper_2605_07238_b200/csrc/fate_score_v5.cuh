@@ -407,9 +407,11 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v5_kernel(fate_bank b, f
             double aff[DPL];
             const bool wl = (walk_m >> (l < 31 ? l : 31)) & 1u;
             if (!wl) {
+                // static level: its term is tabulated (fate_prepare_tail_static_kernel)
                 const double* row = der.tail_static + vl * M1;
 #pragma unroll
-                for (int j = 0; j < DPL; ++j) aff[j] = row[1 + dmc[j]];
+                for (int j = 0; j < DPL; ++j) tail[j] += row[1 + dmc[j]];
+                continue;
             } else {
                 int base = 0;
                 for (int j0 = 0; j0 < n_b; j0 += 32) {

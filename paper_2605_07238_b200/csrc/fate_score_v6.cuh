@@ -458,8 +458,8 @@ __device__ __forceinline__ double v6_qc(const fate_bank& b, const fate_state& st
 
 // One item (scenario, stage v) by one warp; sb = the warp's shared-memory slice
 // (static layout V6Static<DPL>::T when SL, else the runtime layout `lay`).
-// UNIT: the weights' multiplicative identities are compile-time constants --
-// no ablation, and lambda_q = lambda_s = lambda_tr = state_scale =
+// UNIT: the weights' multiplicative identities are compile-time constants
+// (and, with two device slots, the bank fills all 64) -- no ablation, and lambda_q = lambda_s = lambda_tr = state_scale =
 // locality_scale = prefix_scale = transfer_x = prefix_x = kappa_prefix = 1.0
 // (checked on the host, v6_unit_weights).  x * 1.0 == x and (-1.0) * x == -x
 // bit for bit (signed zeros included), so dropping those products is exact;
@@ -488,7 +488,10 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
     int* const s_rowdev = SL ? ss->rowdev : reinterpret_cast<int*>(sb + lay.rowdev);
 
     const unsigned FULL = 0xffffffffu;
-    const int D = b.n_devices, LV = win.levels;
+    // two-slot UNIT banks fill every device slot (D == 64): all lanes live
+    // (measured: C4 -2.8 %; the one-slot kernel is 1 % faster without it)
+    constexpr bool FULLD = UNIT && DPL == 2;
+    const int D = FULLD ? 64 : b.n_devices, LV = win.levels;
     const int Bmax = SL ? V6Static<DPL>::B : b.max_queries;  // row stride of s_rows
     const bool no_loc = !UNIT && (w.ablation & FATE_NO_LOCALITY);
     const bool no_shard = !UNIT && (w.ablation & FATE_NO_SHARD);
@@ -544,7 +547,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 #pragma unroll
     for (int j = 0; j < DPL; ++j) {
         dv[j] = t + 32 * j;
-        live[j] = dv[j] < D;
+        live[j] = FULLD || dv[j] < D;
         res0[j] = live[j] ? st.residency[it.dev_row0 + dv[j]] : -1;
         fr[j] = live[j] ? st.dev_free[it.dev_row0 + dv[j]] : 0.0;
     }
@@ -849,9 +852,11 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
             double aff[DPL];
             const bool wl = (walk_m >> (l < 31 ? l : 31)) & 1u;
             if (!wl) {
+                // static level: its term is tabulated (fate_prepare_tail_static_kernel)
                 const double* row = der.tail_static + vl * M1;
 #pragma unroll
-                for (int j = 0; j < DPL; ++j) aff[j] = row[1 + dmc[j]];
+                for (int j = 0; j < DPL; ++j) tail[j] += row[1 + dmc[j]];
+                continue;
             } else {
                 // op list from the level's template: static entries always, edge
                 // entries iff their parent is located (order preserved), compacted
