@@ -801,12 +801,25 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         }
         // warp min over lanes with a value (min is order-free)
         double cand = have ? bb : __longlong_as_double(0x7ff0000000000000LL);  // +inf
+        const unsigned long long cb = (unsigned long long)__double_as_longlong(cand);
+        // (one device slot per lane: C5 -1 %; the two-slot kernel keeps the
+        // butterfly, +0.5 % with the reductions)
+        if (DPL == 1 && !__any_sync(FULL, (cb >> 63) != 0ull)) {
+            // no negative value and no -0.0: the bit patterns of non-negative
+            // doubles order like the values (and +inf above all finite ones),
+            // so the minimum is two 32-bit warp reductions, high word first
+            const unsigned hi = (unsigned)(cb >> 32);
+            const unsigned mhi = __reduce_min_sync(FULL, hi);
+            const unsigned mlo = __reduce_min_sync(FULL, hi == mhi ? (unsigned)cb : 0xffffffffu);
+            bb = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+        } else {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double y = __shfl_xor_sync(FULL, cand, o);
-            cand = y < cand ? y : cand;
+            for (int o = 16; o > 0; o >>= 1) {
+                const double y = __shfl_xor_sync(FULL, cand, o);
+                cand = y < cand ? y : cand;
+            }
+            bb = cand;
         }
-        bb = cand;
     }
 
     // ---- P3: tail ---------------------------------------------------------------------------------
