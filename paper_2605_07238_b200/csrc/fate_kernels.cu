@@ -378,7 +378,13 @@ template <int DPL, bool SL>
 int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_windows* win,
                  const fate_derived* der, const fate_state* st, const fate_work* work,
                  const fate_out* out, cudaStream_t s) {
-    constexpr int MINB = DPL == 1 ? 10 : 8;
+#ifndef FATE_V6_MINB1
+#define FATE_V6_MINB1 10
+#endif
+#ifndef FATE_V6_MINB2
+#define FATE_V6_MINB2 8
+#endif
+    constexpr int MINB = DPL == 1 ? FATE_V6_MINB1 : FATE_V6_MINB2;
 #ifdef FATE_AB
     switch (ab_env("FATE_MINB", MINB, 1, 16)) {
         case 7: return launch_v6_q<DPL, SL, 7>(bank, w, win, der, st, work, out, s);

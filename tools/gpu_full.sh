@@ -12,5 +12,5 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c5.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 --no-c2 > $O/ncu_l.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fate_score -s 3 -c 1 -o $O/c5_full python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 --no-c2 > $O/ncu_c5.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fate_score -s 3 -c 1 -o $O/c4_full python bench.py --workload c4 --mode sweep --steps 3 --warmup 3 --no-cpu > $O/ncu_c4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fate_score -s 3 -c 1 -o $O/c4_full python bench.py --workload c4 --mode sweep --steps 3 --warmup 3 --no-cpu --no-c2 > $O/ncu_c4.log 2>&1
 ls -la $O
