@@ -38,7 +38,8 @@ def main():
         db = runtime.DeviceBank(bank, cfg.weights, device=dev)
         ds, dw = db.upload_states(states), db.upload_work(work)
         o = db.alloc_out(work, extras=True)
-        o.tail = None
+        if not os.environ.get("KB_TAIL"):
+            o.tail = None
         if os.environ.get("KB_NO_SCHED"):
             o.sched = None
         ms = []
