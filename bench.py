@@ -95,10 +95,16 @@ def shard_plan(rank: int, world: int, total: int = TOTAL_INSTANCES,
             "scaling": scaling}
 
 
-def c4_plan(rank: int, world: int, n_scen: int = C4_SCENARIOS) -> tuple:
-    """Config-4 scenario seeds of a rank: contiguous ranges of n_scen/world."""
-    lo, hi = rank * n_scen // world, (rank + 1) * n_scen // world
-    return lo, hi - lo
+def c4_plan(rank: int, world: int, n_scen: int = C4_SCENARIOS) -> dict:
+    """Config-4 work items of a rank ("split S scenarios (or the
+    10k stages)"): every scenario seed, the stages v with v = rank (mod world).
+    The static DAG and the 8 scenario states are replicated on every rank.
+    Splitting by scenario seeds instead is unbalanced: the walk work of a
+    scenario grows with its located depth (scenario 4 holds 22 % of the C4
+    sweep's walked levels, scenario 1 4 %), and the stage index follows the
+    level bands (lexicographic ids), so contiguous stage ranges are unbalanced
+    too; the residue classes mix every level of every scenario."""
+    return {"first": 0, "count": n_scen, "stage_rank": rank, "stage_world": world}
 
 
 def reduce_max(value: float, world: int, device=None) -> float:
@@ -238,10 +244,12 @@ def build_c5(plan: dict, mode: str):
     return cfg, fb.bank, fb.states, work
 
 
-def build_c4(mode: str = "sweep", n_scen: int = C4_SCENARIOS, first_scen: int = 0):
+def build_c4(mode: str = "sweep", n_scen: int = C4_SCENARIOS, first_scen: int = 0,
+             stage_rank: int = 0, stage_world: int = 1):
     """Config 4 from the native generator: one 10k-stage instance (seed 1),
-    scenario states s = first_scen .. first_scen+n_scen-1 (ranks shard the
-    scenario seeds)."""
+    scenario states s = first_scen .. first_scen+n_scen-1; the work items are
+    the (scenario, stage v) pairs with v = stage_rank (mod stage_world) (a
+    rank's share, c4_plan)."""
     import numpy as np
 
     from paper_2605_07238_b200 import fastgen, pack, scenarios
@@ -268,10 +276,11 @@ def build_c4(mode: str = "sweep", n_scen: int = C4_SCENARIOS, first_scen: int = 
     items = []
     for s, p in enumerate(parts):
         if mode == "sweep":
-            items += [(s, g) for g in range(V)]
+            gs = range(stage_rank, V, stage_world)
         else:
             _, g = p.frontier_items()
-            items += [(s, int(x)) for x in g]
+            gs = [int(x) for x in g if int(x) % stage_world == stage_rank]
+        items += [(s, g) for g in gs]
     work = pack.make_work(bank, items, cfg.weights.ablation.no_shard)
     return cfg, bank, states, work
 
@@ -290,8 +299,8 @@ def workload_config(args, world: int) -> dict:
     return {"workload": f"c4_{args.mode}", "instances": 1, "stages_per_instance": 10000,
             "devices": 64, "batch": 16, "horizon": 4, "scenario_states": C4_SCENARIOS,
             "l2": "flushed between steps (256 MiB write, outside the events)",
-            "parallelism": f"dp{world}: scenario seeds {C4_SCENARIOS}/{world} per rank "
-                           "(strong scaling)"}
+            "parallelism": f"dp{world}: stages v = rank (mod {world}) of all "
+                           f"{C4_SCENARIOS} scenario seeds per rank (strong scaling)"}
 
 
 def cpu_model() -> str:
@@ -702,9 +711,11 @@ def run_fate(args):
         plan = shard_plan(rank, world, scaling="strong")
         cfg, bank, states, work = build_c5(plan, args.mode)
     else:
-        first, n_scen = c4_plan(rank, world)
-        cfg, bank, states, work = build_c4(args.mode, n_scen=n_scen, first_scen=first)
-        plan = {"first": first, "count": n_scen}
+        plan = c4_plan(rank, world)
+        cfg, bank, states, work = build_c4(args.mode, n_scen=plan["count"],
+                                           first_scen=plan["first"],
+                                           stage_rank=plan["stage_rank"],
+                                           stage_world=plan["stage_world"])
     nvtx.range_pop()
 
     cpu = None
@@ -1011,8 +1022,10 @@ def measure_api_waves() -> dict | None:
 def measure_c4(torch, device, args, rank: int = 0, world: int = 1) -> dict:
     from paper_2605_07238_b200 import pack, runtime
 
-    first, n_scen = c4_plan(rank, world)
-    cfg, bank, states, work = build_c4("sweep", n_scen=n_scen, first_scen=first)
+    plan = c4_plan(rank, world)
+    cfg, bank, states, work = build_c4("sweep", n_scen=plan["count"], first_scen=plan["first"],
+                                       stage_rank=plan["stage_rank"],
+                                       stage_world=plan["stage_world"])
     dbank = runtime.DeviceBank(bank, cfg.weights, device=device)
     dstates = dbank.upload_states(states)
     dwork = dbank.upload_work(work)
@@ -1026,7 +1039,7 @@ def measure_c4(torch, device, args, rank: int = 0, world: int = 1) -> dict:
     tot = reduce_sum(float(work.n_psi), world, device)
     cs = clocks.summary()
     return {"workload": "c4_sweep (10k stages x 8 scenarios, 64 devices, 8 models, H=4; "
-                        f"scenarios {C4_SCENARIOS}/{world} per rank)",
+                        f"per rank: stages v = rank (mod {world}) of every scenario)",
             "value": tot / (ms_max / 1e3), "unit": UNIT, "ms_per_step": ms_max,
             "psi_per_step": tot,
             "roofline": _roofline(pack, runtime, bank, work, states, dbank, ms, "c4_sweep",

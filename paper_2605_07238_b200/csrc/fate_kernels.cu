@@ -288,19 +288,22 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
         occ_dev = dev;
         occ_fn = fn;
     }
-    // items per ticket: 2 for one device slot per lane, 1 for two (heavier
-    // items: finer tail balance beats fewer atomics).  Measured on B200 at
-    // the current register budgets (A/B: 0 = guided sizes).
-#ifdef FATE_AB
-    static const int fetch_env = ab_env("FATE_V6_FETCH", -1, 0, 64);
-    const int fetch = fetch_env >= 0 ? fetch_env : (DPL == 1 ? 2 : 1);
-#else
-    const int fetch = DPL == 1 ? 2 : 1;
-#endif
     if (work->n_items > 0x7fffffffLL - 4 * 128 * 64)
         return fail(FATE_ETOOBIG, "v6: too many items for the 32-bit ticket counter");
     const long long want = (work->n_items + 3) / 4;
     const unsigned blocks = (unsigned)std::min<long long>(o, want);
+    // items per ticket: 2 for one device slot per lane on batches of >= 3
+    // items per warp, else 1 (heavier items, or small shards -- 2 items per
+    // warp at config 5's 8-way shard: finer tail balance beats fewer
+    // atomics).  Measured on B200 at the current register budgets (A/B: 0 =
+    // guided sizes).
+    const int fetch_dflt = (DPL == 1 && work->n_items >= 3LL * 4 * blocks) ? 2 : 1;
+#ifdef FATE_AB
+    static const int fetch_env = ab_env("FATE_V6_FETCH", -1, 0, 64);
+    const int fetch = fetch_env >= 0 ? fetch_env : fetch_dflt;
+#else
+    const int fetch = fetch_dflt;
+#endif
     static std::atomic<int> slot{0};
     const int qs = g_queue_slot_override >= 0 ? g_queue_slot_override
                                               : slot.fetch_add(1) % V6_QDIRECT;
@@ -390,6 +393,8 @@ int launch_v6_sl(const fate_bank* bank, const fate_weights* w, const fate_window
         case 7: return launch_v6_q<DPL, SL, 7>(bank, w, win, der, st, work, out, s);
         case 8: return launch_v6_q<DPL, SL, 8>(bank, w, win, der, st, work, out, s);
         case 10: return launch_v6_q<DPL, SL, 10>(bank, w, win, der, st, work, out, s);
+        case 12: return launch_v6_q<DPL, SL, 12>(bank, w, win, der, st, work, out, s);
+        case 16: return launch_v6_q<DPL, SL, 16>(bank, w, win, der, st, work, out, s);
         default: break;
     }
 #endif

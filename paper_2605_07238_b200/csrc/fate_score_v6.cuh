@@ -1234,7 +1234,15 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
     // 1/(4 * warps) of what the warp last saw remaining (at least one), so
     // early tickets are large (few atomics) and late ones single items (tail
     // balance)
-    const float inv_share = 0.25f / (float)(gridDim.x * (blockDim.x >> 5));
+    const unsigned nw = gridDim.x * (blockDim.x >> 5);
+    const float inv_share = 0.25f / (float)nw;
+    // first ticket without the atomic: warp g takes items [g f0, (g+1) f0);
+    // the counter hands out the items from nw f0 on (an atomic round trip
+    // less on every warp's critical path -- it matters when each warp scores
+    // only a few items, i.e. small shards)
+    const unsigned f0 = fetch > 0 ? (unsigned)fetch : 1u;
+    const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (unsigned)wi;
+    bool first = true;
     long long seen = 0;
     for (;;) {
         long long take = fetch;
@@ -1242,12 +1250,19 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
             take = (long long)((float)(n - seen) * inv_share);
             take = take < 1 ? 1 : (take > 16 ? 16 : take);
         }
-        unsigned int i = 0;
-        if (t == 0) i = atomicAdd(q, (unsigned)take);
-        i = __shfl_sync(0xffffffffu, i, 0);
-        seen = (long long)i + take;
-        if ((long long)i >= n) break;
-        const long long i1 = (long long)i + take < n ? (long long)i + take : n;
+        long long i;
+        if (first) {
+            take = f0;
+            i = (long long)gw * f0;
+            first = false;
+        } else {
+            unsigned int k = 0;
+            if (t == 0) k = atomicAdd(q, (unsigned)take);
+            i = (long long)__shfl_sync(0xffffffffu, k, 0) + (long long)nw * f0;
+        }
+        seen = i + take;
+        if (i >= n) break;
+        const long long i1 = i + take < n ? i + take : n;
 #pragma unroll 1
         for (long long it = i; it < i1; ++it) {
             v6_item<DPL, OVR, SL, QG, UNIT>(b, w, win, der, st, work, out, lay, it, sb);

@@ -99,8 +99,9 @@ def test_two_rank_plan_gathers_and_solves():
         for r in range(2):
             assert np.array_equal(rank_out[5][r].view(np.uint64), out[r][4].view(np.uint64))
             assert np.array_equal(rank_out[7][r], out[r][6])
-    # C4 scenario split covers 0..7 disjointly
-    assert (r0[9], r1[9]) == ((0, 4), (4, 4))
+    # C4: every scenario on every rank, stages split by residue mod world
+    assert r0[9] == {"first": 0, "count": 8, "stage_rank": 0, "stage_world": 2}
+    assert r1[9] == {"first": 0, "count": 8, "stage_rank": 1, "stage_world": 2}
     # the union equals one process doing the whole batch
     psi_all, _, sel_all, _, _ = _shard(bench.shard_plan(0, 1, total=TOTAL))
     assert np.array_equal(np.concatenate([r0[4], r1[4]]).view(np.uint64),
