@@ -903,7 +903,6 @@ def measure_c2_runs() -> dict | None:
     t0 = time.perf_counter()
     recs["reference"] = [RE.run(RP.make_policy("fate"), reg[k], cfg) for k in keys]
     out["reference_python_s"] = time.perf_counter() - t0
-    scorer = GpuScorer()
     # untimed warm-up run per GPU mode (CUDA context, library, allocator pools)
     RE.run(FateGpuPolicy(scorer=GpuScorer()), reg[keys[0]], cfg)
     m0 = MirrorScorer(gpu_frontier=True)
@@ -912,35 +911,56 @@ def measure_c2_runs() -> dict | None:
         RE.run(FateGpuPolicy(scorer=m0), reg[keys[0]], cfg)
     finally:
         compat.uninstall()
-    pols = []
-    t0 = time.perf_counter()
-    rr = []
-    for k in keys:
-        pol = FateGpuPolicy(scorer=scorer)
-        rr.append(RE.run(pol, reg[k], cfg))
-        pols.append(pol)
-    out["gpu_policy_s"] = time.perf_counter() - t0
+
+    def gpu_policy_pass():
+        scorer = GpuScorer()  # bank setup (pack + upload per instance) inside the pass
+        pols, rr = [], []
+        t0 = time.perf_counter()
+        for k in keys:
+            pol = FateGpuPolicy(scorer=scorer)
+            rr.append(RE.run(pol, reg[k], cfg))
+            pols.append(pol)
+        return time.perf_counter() - t0, rr, pols, scorer
+
+    def mirror_pass():
+        rr = []
+        t0 = time.perf_counter()
+        for k in keys:
+            m = MirrorScorer(gpu_frontier=True)
+            compat.install(mirror=m, policy_factory=False, durations=True)
+            try:
+                rr.append(RE.run(FateGpuPolicy(scorer=m), reg[k], cfg))
+            finally:
+                compat.uninstall()
+        return time.perf_counter() - t0, rr
+
+    # three interleaved passes per GPU mode, median reported: a pass of tiny
+    # waves is sensitive to the box (GPU power state after idle, host
+    # scheduling), the reference pass (CPU only) is not
+    pol_s, mir_s, pol_runs = [], [], []
+    for _ in range(3):
+        dt, rr, pols, scorer = gpu_policy_pass()
+        pol_s.append(dt)
+        pol_runs.append((dt, rr, pols, scorer))
+        dt, rr_m = mirror_pass()
+        mir_s.append(dt)
+    dt, rr, pols, scorer = sorted(pol_runs, key=lambda x: x[0])[1]
+    out["gpu_policy_s"] = dt
+    out["gpu_policy_s_passes"] = pol_s
     recs["gpu"] = rr
     out["waves"] = int(sum(p.solver_stats.solves for p in pols))
     out["gpu_score_s"] = float(sum(p.score_seconds for p in pols))
     out["gpu_bank_setup_s"] = float(scorer.bank_seconds)
     out["gpu_score_ms_per_wave_excl_bank_setup"] = round(
         1e3 * (out["gpu_score_s"] - scorer.bank_seconds) / max(1, out["waves"]), 4)
-    t0 = time.perf_counter()
-    rr = []
-    for k in keys:
-        m = MirrorScorer(gpu_frontier=True)
-        compat.install(mirror=m, policy_factory=False, durations=True)
-        try:
-            rr.append(RE.run(FateGpuPolicy(scorer=m), reg[k], cfg))
-        finally:
-            compat.uninstall()
-    out["gpu_mirror_durations_s"] = time.perf_counter() - t0
-    recs["mirror"] = rr
+    out["gpu_mirror_durations_s"] = sorted(mir_s)[1]
+    out["gpu_mirror_durations_s_passes"] = mir_s
+    recs["mirror"] = rr_m
     want = [rec_key(r) for r in recs["reference"]]
     out["identical_records"] = all([rec_key(r) for r in recs[n]] == want for n in ("gpu", "mirror"))
     out["note"] = ("wall clock of whole runs (executor, solve, fill, materialise included; "
-                   "one untimed warm-up run per GPU mode first); the snapshot policy scores "
+                   "one untimed warm-up run per GPU mode first; GPU modes: median of three "
+                   "interleaved passes, all listed); the snapshot policy scores "
                    "each wave with one H2D copy, one launch and one D2H copy "
                    "(runtime.WaveRunner); bank setup = packing + uploading each instance once; "
                    "the rest of a run is the caller's own solver and executor")
