@@ -338,6 +338,13 @@ __device__ __forceinline__ double v6_qc_value(long long stage_part, long long qu
 // helpers
 // ---------------------------------------------------------------------------
 
+// The walk's conditional add.  `@p add.rn.f64` in PTX is if-converted by
+// ptxas into an unconditional DADD plus a two-word FSEL (4 SASS per op and
+// device slot); a branch around the add is compiled to a predicated DADD
+// instead (LOP3 -> P, @!P DADD: 2 SASS per op and slot, against 3 for the
+// exact 0/1-factor FMA of the previous generation).  A skipped op leaves the
+// accumulator untouched, exactly as the reference, which never evaluates it.
+
 // aff_j += val for every device slot j that the op applies to:
 //   key <  1000: applies unless key == device (key 999 = every device)
 //   key >= 1000: applies iff key == tgt_j (= 1000 + displaced resident model)
@@ -345,7 +352,9 @@ template <int DPL>
 __device__ __forceinline__ void v6_apply(double (&aff)[DPL], double val, int k, const int (&d)[DPL],
                                          const int (&tgt)[DPL]) {
     if (DPL == 1) {
-        // 0/1-factor FMA form (see v6_apply_m): same bits as the predicated add
+        // one device slot: the exact 0/1-factor FMA (fma(v, 1, a) = RN(v + a),
+        // fma(v, 0, a) = a for finite v and a chain that is never -0.0) -- on
+        // the one-slot kernel the predicated form measured 2 % slower (C5)
         asm("{\n\t// fate-fma01\n\t.reg .pred q, p;\n\t.reg .b32 h;\n\t.reg .f64 f;\n\t"
             "setp.lt.s32 q, %2, 1000;\n\t"
             "setp.ne.and.s32 p, %2, %3, q;\n\t"
@@ -356,22 +365,27 @@ __device__ __forceinline__ void v6_apply(double (&aff)[DPL], double val, int k, 
             : "+d"(aff[0])
             : "d"(val), "r"(k), "r"(d[0]), "r"(tgt[0]));
     } else {
-        asm("{\n\t.reg .pred q, p, r;\n\t"
-            "setp.lt.s32 q, %3, 1000;\n\t"
-            "setp.ne.and.s32 p, %3, %4, q;\n\t"
-            "setp.eq.or.s32 p, %3, %6, p;\n\t"
-            "setp.ne.and.s32 r, %3, %5, q;\n\t"
-            "setp.eq.or.s32 r, %3, %7, r;\n\t"
-            "@p add.rn.f64 %0, %0, %2;\n\t"
-            "@r add.rn.f64 %1, %1, %2;\n\t}"
-            : "+d"(aff[0]), "+d"(aff[DPL - 1])
-            : "d"(val), "r"(k), "r"(d[0]), "r"(d[DPL - 1]), "r"(tgt[0]), "r"(tgt[DPL - 1]));
+        asm volatile("{\n\t.reg .pred q, p, r;\n\t"
+                     "setp.lt.s32 q, %3, 1000;\n\t"
+                     "setp.ne.and.s32 p, %3, %4, q;\n\t"
+                     "setp.eq.or.s32 p, %3, %6, p;\n\t"
+                     "setp.ne.and.s32 r, %3, %5, q;\n\t"
+                     "setp.eq.or.s32 r, %3, %7, r;\n\t"
+                     "@!p bra V6A%=;\n\t"
+                     "add.rn.f64 %0, %0, %2;\n\t"
+                     "V6A%=:\n\t"
+                     "@!r bra V6B%=;\n\t"
+                     "add.rn.f64 %1, %1, %2;\n\t"
+                     "V6B%=:\n\t}"
+                     : "+d"(aff[0]), "+d"(aff[DPL - 1])
+                     : "d"(val), "r"(k), "r"(d[0]), "r"(d[DPL - 1]), "r"(tgt[0]),
+                       "r"(tgt[DPL - 1]));
     }
 }
 
 // Masked op of the non-override walk: the op applies to device t (t + 32)
-// iff bit t of lo (hi) is set -- one bit test per device slot, then the same
-// predicated add.rn.f64 as v6_apply.
+// iff bit t of lo (hi) is set -- one bit test (LOP3 with a predicate output)
+// and one predicated DADD per device slot.
 template <int DPL>
 __device__ __forceinline__ void v6_apply_m(double (&aff)[DPL], double val, unsigned lo,
                                            unsigned hi, unsigned lanebit) {
@@ -383,27 +397,19 @@ __device__ __forceinline__ void v6_apply_m(double (&aff)[DPL], double val, unsig
             : "+d"(aff[0])
             : "d"(val), "r"(lo), "r"(lanebit));
     } else {
-        // 0/1 factor form: aff = fma(val, f, aff) with f = +1.0 or +0.0 selected
-        // on its high word.  fma(v, 1, a) = RN(v + a) is the add itself and
-        // fma(v, 0, a) = RN(+-0 + a) = a since the chain is never -0.0 -- the
-        // same bits as the predicated add, with one select instead of the two
-        // ptxas emits to if-convert it (B200: 95 vs 80 G warp-ops/s,
-        // tools/issue_probe.cu).  The marker lets build.py's contraction
-        // check tell this exact FMA from a contracted a*b+c.
-        asm("{\n\t// fate-fma01\n\t.reg .pred p, r;\n\t.reg .b32 x, y, hx, hy;\n\t"
-            ".reg .f64 f, g;\n\t"
-            "and.b32 x, %3, %5;\n\t"
-            "and.b32 y, %4, %5;\n\t"
-            "setp.ne.b32 p, x, 0;\n\t"
-            "setp.ne.b32 r, y, 0;\n\t"
-            "selp.b32 hx, 0x3ff00000, 0, p;\n\t"
-            "selp.b32 hy, 0x3ff00000, 0, r;\n\t"
-            "mov.b64 f, {0, hx};\n\t"
-            "mov.b64 g, {0, hy};\n\t"
-            "fma.rn.f64 %0, %2, f, %0;\n\t"
-            "fma.rn.f64 %1, %2, g, %1;\n\t}"
-            : "+d"(aff[0]), "+d"(aff[DPL - 1])
-            : "d"(val), "r"(lo), "r"(hi), "r"(lanebit));
+        asm volatile("{\n\t.reg .pred p, r;\n\t.reg .b32 x, y;\n\t"
+                     "and.b32 x, %3, %5;\n\t"
+                     "and.b32 y, %4, %5;\n\t"
+                     "setp.eq.b32 p, x, 0;\n\t"
+                     "setp.eq.b32 r, y, 0;\n\t"
+                     "@p bra V6M%=;\n\t"
+                     "add.rn.f64 %0, %0, %2;\n\t"
+                     "V6M%=:\n\t"
+                     "@r bra V6N%=;\n\t"
+                     "add.rn.f64 %1, %1, %2;\n\t"
+                     "V6N%=:\n\t}"
+                     : "+d"(aff[0]), "+d"(aff[DPL - 1])
+                     : "d"(val), "r"(lo), "r"(hi), "r"(lanebit));
     }
 }
 
@@ -610,7 +616,11 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         }
     }
     // v's parents: lane-parallel fetch, broadcast in ascending order
-    // (transfer_cost, costs.py:113-125; colo counts, costs.py:160-165)
+    // (transfer_cost, costs.py:113-125; colo counts, costs.py:160-165).
+    // Under unit weights without overrides the prologue's edge term
+    // lambda_tr * beta * sigma * transfer_x * locality_scale is beta * sigma
+    // bit for bit (x * 1.0 == x), so the product is read, not recomputed.
+    constexpr bool TERM = UNIT && !OVR;
     #pragma unroll 1
     for (int e0 = pa0; e0 < pa1; e0 += 32) {
         const int e = e0 + t;
@@ -618,7 +628,7 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
         double sg = 0.0;
         if (e < pa1) {
             L = loc_row[b.par_idx[e]];
-            sg = der.edge_sigma[e];
+            sg = TERM ? der.edge_term[e] : der.edge_sigma[e];
         }
         const int n = pa1 - e0 < 32 ? pa1 - e0 : 32;
         #pragma unroll 1
@@ -629,9 +639,11 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 #pragma unroll
             for (int j = 0; j < DPL; ++j) {
                 hit[j] += Li == dv[j];
-                if (live[j] && Li != dv[j]) {
-                    const double beta = OVR ? b.beta[(size_t)Li * D + dv[j]] : b.beta_default;
-                    trv[j] += beta * si;
+                if (OVR) {
+                    if (live[j] && Li != dv[j])
+                        trv[j] += b.beta[(size_t)Li * D + dv[j]] * si;
+                } else {
+                    if (live[j] && Li != dv[j]) trv[j] += TERM ? si : b.beta_default * si;
                 }
             }
         }
