@@ -22,13 +22,15 @@
 //    index and is kept iff that parent is located in the scenario -- so a
 //    level's op list is built with one coalesced 16-byte load and one loc
 //    gather per 32 entries plus a ballot compaction, no nested parent loops;
-//  * op walk with predicated adds (inline PTX: two predicate-combining setp
-//    and one predicated add.rn.f64 per device slot; with two device slots per
+//  * op walk with conditional adds in inline PTX.  With two device slots per
 //    lane and no overrides each buffered op carries the 64-bit mask of the
-//    devices it applies to, so the predicate is one bit test).  Skipping an
-//    op equals adding +0.0 exactly because the chain starts at +0.0 and never
-//    becomes -0.0 in round-to-nearest (v5's argument), so this is v5's chain
-//    bit for bit;
+//    devices it applies to, and an (op, slot) is one bit test and one
+//    predicated DADD (a branch around add.rn.f64, which ptxas keeps as
+//    @P DADD); a skipped op leaves the chain untouched.  One slot per lane
+//    walks op keys (three predicate-combining setp) with the exact 0/1-factor
+//    FMA (skipping = adding +0.0, exact because the chain starts at +0.0 and
+//    never becomes -0.0 in round-to-nearest).  Both are v5's chain bit for
+//    bit;
 //  * op lists compacted and walked in chunks through a small per-warp buffer
 //    (order preserved), so shared memory does not grow with the longest
 //    template and the L1 carve-out stays large;
