@@ -898,60 +898,110 @@ __device__ __forceinline__ void v6_item(const fate_bank& b, const fate_weights& 
 #pragma unroll
                 for (int j = 0; j < DPL; ++j) aff[j] = 0.0;
                 long long j0 = t0;
+                // two device slots: 32-bit level-relative indices and
+                // branch-free entries (an edge's location gather is
+                // predicated, the static masks are selected)
+                const V6Op* const lvt = tmpl + t0;
+                const int cnt = (int)(t1 - t0);
+                int k0 = 0;
+                unsigned lt_mask;
+                asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt_mask));
                 #pragma unroll 1
-                while (j0 < t1) {
+                while (MASKW ? k0 < cnt : j0 < t1) {
                     // compact template blocks until the buffer could overflow
                     int base = 0;
-                    #pragma unroll 1
-                    do {
-                        const long long jx = j0 + t;
-                        bool keep = false;
-                        double val = 0.0;
-                        unsigned mlo = 0u, mhi = 0u;
-                        if (jx < t1) {
-                            const int4 raw = __ldg(reinterpret_cast<const int4*>(tmpl + jx));
-                            val = __hiloint2double(raw.y, raw.x);
-                            if (raw.z < 0) {
-                                keep = true;
-                                if (!MASKW) {
-                                    mlo = (unsigned)raw.w;
-                                } else if (raw.w == V6_KEY_ALWAYS) {
-                                    mlo = mhi = ~0u;
+                    if (MASKW) {
+                        #pragma unroll 1
+                        do {
+                            const int k = k0 + t;
+                            bool keep = false;
+                            double val = 0.0;
+                            unsigned mlo = 0u, mhi = 0u;
+                            if (k < cnt) {
+                                const int4 raw = __ldg(reinterpret_cast<const int4*>(lvt + k));
+                                val = __hiloint2double(raw.y, raw.x);
+                                const bool edge = raw.z >= 0;
+#ifdef FATE_AB
+                                const int L = !edge ? -1
+                                              : (lay.diag & 8) ? (raw.z & 1) - 1 + (raw.z & 2)
+                                                               : loc_row[raw.z];
+#else
+                                const int L = edge ? loc_row[raw.z] : -1;
+#endif
+                                const int mx = raw.w - V6_KEY_MODEL;
+                                const bool disp = !edge && raw.w != V6_KEY_ALWAYS;
+                                unsigned slo = ~0u, shi = ~0u;
+                                if (disp) {
+                                    const bool known = mx < b.n_models;
+                                    slo = known ? s_mm[2 * mx] : 0u;
+                                    shi = known ? s_mm[2 * mx + 1] : 0u;
+                                }
+                                const unsigned nb = ~(1u << (L & 31));
+                                mlo = edge ? (L < 32 ? nb : ~0u) : slo;
+                                mhi = edge ? (L >= 32 ? nb : ~0u) : shi;
+                                keep = !edge || L >= 0;
+                            }
+                            const unsigned bal = __ballot_sync(FULL, keep);
+                            if (keep) {
+                                const int pos = base + __popc(bal & lt_mask);
+                                s_opval[pos] = val;
+                                s_opmask[pos] = make_uint2(mlo, mhi);
+                            }
+                            base += __popc(bal);
+                            k0 += 32;
+                        } while (k0 < cnt && base + 32 <= lay.ops_cap);
+                    } else {
+                        #pragma unroll 1
+                        do {
+                            const long long jx = j0 + t;
+                            bool keep = false;
+                            double val = 0.0;
+                            unsigned mlo = 0u, mhi = 0u;
+                            if (jx < t1) {
+                                const int4 raw = __ldg(reinterpret_cast<const int4*>(tmpl + jx));
+                                val = __hiloint2double(raw.y, raw.x);
+                                if (raw.z < 0) {
+                                    keep = true;
+                                    if (!MASKW) {
+                                        mlo = (unsigned)raw.w;
+                                    } else if (raw.w == V6_KEY_ALWAYS) {
+                                        mlo = mhi = ~0u;
+                                    } else {
+                                        const int mx = raw.w - V6_KEY_MODEL;
+                                        if (mx < b.n_models) {
+                                            mlo = s_mm[2 * mx];
+                                            mhi = s_mm[2 * mx + 1];
+                                        }
+                                    }
                                 } else {
-                                    const int mx = raw.w - V6_KEY_MODEL;
-                                    if (mx < b.n_models) {
-                                        mlo = s_mm[2 * mx];
-                                        mhi = s_mm[2 * mx + 1];
+#ifdef FATE_AB
+                                    const int L = (lay.diag & 8) ? (raw.z & 1) - 1 + (raw.z & 2)
+                                                                 : loc_row[raw.z];
+#else
+                                    const int L = loc_row[raw.z];
+#endif
+                                    keep = L >= 0;
+                                    if (!MASKW) {
+                                        mlo = (unsigned)(OVR ? V6_KEY_SIGMA + L : L);
+                                    } else {
+                                        mlo = L < 32 ? ~(1u << (L & 31)) : ~0u;
+                                        mhi = L >= 32 ? ~(1u << (L & 31)) : ~0u;
                                     }
                                 }
-                            } else {
-#ifdef FATE_AB
-                                const int L = (lay.diag & 8) ? (raw.z & 1) - 1 + (raw.z & 2)
-                                                             : loc_row[raw.z];
-#else
-                                const int L = loc_row[raw.z];
-#endif
-                                keep = L >= 0;
-                                if (!MASKW) {
-                                    mlo = (unsigned)(OVR ? V6_KEY_SIGMA + L : L);
-                                } else {
-                                    mlo = L < 32 ? ~(1u << (L & 31)) : ~0u;
-                                    mhi = L >= 32 ? ~(1u << (L & 31)) : ~0u;
-                                }
                             }
-                        }
-                        const unsigned bal = __ballot_sync(FULL, keep);
-                        if (keep) {
-                            const int pos = base + __popc(bal & ((1u << t) - 1u));
-                            s_opval[pos] = val;
-                            if (MASKW)
-                                s_opmask[pos] = make_uint2(mlo, mhi);
-                            else
-                                s_opkey[pos] = (int)mlo;
-                        }
-                        base += __popc(bal);
-                        j0 += 32;
-                    } while (j0 < t1 && base + 32 <= lay.ops_cap);
+                            const unsigned bal = __ballot_sync(FULL, keep);
+                            if (keep) {
+                                const int pos = base + __popc(bal & ((1u << t) - 1u));
+                                s_opval[pos] = val;
+                                if (MASKW)
+                                    s_opmask[pos] = make_uint2(mlo, mhi);
+                                else
+                                    s_opkey[pos] = (int)mlo;
+                            }
+                            base += __popc(bal);
+                            j0 += 32;
+                        } while (j0 < t1 && base + 32 <= lay.ops_cap);
+                    }
                     // walk the buffered chunk
 #ifdef FATE_AB
                     if (lay.diag & 4) {
