@@ -344,3 +344,25 @@ def test_wave_packer_equals_pack_states(which):
         got = v["kappa"].reshape(D, cap, 4)[:, : ref.kappa_cap]
         assert np.array_equal(got, ref.arrays["kappa"].reshape(D, ref.kappa_cap, 4))
         assert not v["kappa"].reshape(D, cap, 4)[:, ref.kappa_cap:].any()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_c4_rank_shares_partition_the_sweep(world):
+    """bench.c4_plan / build_c4: the ranks' (scenario, stage)
+    work items are disjoint and together are exactly the single-process
+    sweep, in the same per-rank order (scenario-major, ascending stage)."""
+    import bench
+
+    _, _, _, full = bench.build_c4("sweep", n_scen=2)
+    want = set(zip(full.scen.tolist(), full.stage.tolist()))
+    got = []
+    for r in range(world):
+        p = bench.c4_plan(r, world, n_scen=2)
+        _, _, _, w = bench.build_c4("sweep", n_scen=p["count"], first_scen=p["first"],
+                                    stage_rank=p["stage_rank"], stage_world=p["stage_world"])
+        items = list(zip(w.scen.tolist(), w.stage.tolist()))
+        assert items == sorted(items)
+        assert all(g % world == r for _, g in items)
+        got += items
+    assert len(got) == len(set(got)) == len(want)
+    assert set(got) == want

@@ -15,7 +15,7 @@ cfg, bank, states, work = bench.build_c5(bench.shard_plan(0, 1), "frontier")
 dbank = runtime.DeviceBank(bank, cfg.weights, device=dev)
 for chunks in [int(x) for x in sys.argv[1:]] or [4]:
     pipe = runtime.HostPipeline(dbank, states, work, n_chunks=chunks, graph=True)
-    ms, blocks = bench.time_e2e(torch, pipe, 50, 3, 1, dev)
+    ms, blocks = bench.time_e2e(torch, pipe.run, 50, 3, 1, dev)
     print(json.dumps({"chunks": chunks, "first": os.environ.get("FATE_PIPE_FIRST"), "ms": ms,
                       "blocks": [round(b, 3) for b in blocks]}), flush=True)
     pipe.close()
