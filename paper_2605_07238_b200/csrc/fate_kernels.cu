@@ -292,12 +292,13 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
         return fail(FATE_ETOOBIG, "v6: too many items for the 32-bit ticket counter");
     const long long want = (work->n_items + 3) / 4;
     const unsigned blocks = (unsigned)std::min<long long>(o, want);
-    // items per ticket: 2 for one device slot per lane on batches of >= 3
-    // items per warp, else 1 (heavier items, or small shards -- 2 items per
-    // warp at config 5's 8-way shard: finer tail balance beats fewer
-    // atomics).  Measured on B200 at the current register budgets (A/B: 0 =
-    // guided sizes).
-    const int fetch_dflt = (DPL == 1 && work->n_items >= 3LL * 4 * blocks) ? 2 : 1;
+    // items per ticket, one device slot per lane: 3 on batches of >= 8 items
+    // per warp, 2 on >= 3, else 1; two slots: 1 (heavier items, or small
+    // shards -- 2 items per warp at config 5's 8-way shard: finer tail
+    // balance beats fewer atomics).  Measured on B200 at the current
+    // register budgets (A/B: 0 = guided sizes).
+    const long long per_warp = work->n_items / (4LL * blocks);
+    const int fetch_dflt = DPL != 1 ? 1 : per_warp >= 8 ? 3 : per_warp >= 3 ? 2 : 1;
 #ifdef FATE_AB
     static const int fetch_env = ab_env("FATE_V6_FETCH", -1, 0, 64);
     const int fetch = fetch_env >= 0 ? fetch_env : fetch_dflt;
