@@ -1305,11 +1305,15 @@ __global__ void __launch_bounds__(128, MINB) fate_score_v6_kernel(fate_bank b, f
     // balance)
     const unsigned nw = gridDim.x * (blockDim.x >> 5);
     const float inv_share = 0.25f / (float)nw;
-    // first ticket without the atomic: warp g takes items [g f0, (g+1) f0);
-    // the counter hands out the items from nw f0 on (an atomic round trip
-    // less on every warp's critical path -- it matters when each warp scores
-    // only a few items, i.e. small shards)
-    const unsigned f0 = fetch > 0 ? (unsigned)fetch : 1u;
+    // first ticket without the atomic: warp g takes items [g f0, (g+1) f0)
+    // (f0 = the launch's static first share, else one ticket); the counter
+    // hands out the items from nw f0 on (an atomic round trip less on every
+    // warp's critical path -- it matters when each warp scores only a few
+    // items, i.e. small shards)
+    // fetch = items per ticket | (items of the static first ticket << 8)
+    const unsigned first_take = (unsigned)fetch >> 8;
+    fetch &= 0xff;
+    const unsigned f0 = first_take ? first_take : (fetch > 0 ? (unsigned)fetch : 1u);
     const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (unsigned)wi;
     bool first = true;
     long long seen = 0;
