@@ -305,14 +305,14 @@ int launch_v6_mb(const fate_bank* bank, const fate_weights* w, const fate_window
 #else
     const int fetch = fetch_dflt;
 #endif
-    // static first share on batches of >= 8 items per warp: each warp first
+    // static first share on batches of >= 3 items per warp: each warp first
     // scores a contiguous run of its share (no atomics, one scenario's rows
     // stay in L1), then pulls tickets.  3/4 of the share for one device slot
     // (config-5 items cost alike), 1/2 for two (config-4 items vary with
-    // their walked levels).  Measured on B200: C5 -3 %, C4 -1.5 %; larger
-    // static shares made C4 up to 25 % slower, the whole share made both
-    // slower.
-    const long long first_take = per_warp < 8 ? 0 : DPL == 1 ? per_warp * 3 / 4 : per_warp / 2;
+    // their walked levels).  Measured on B200: C5 -3 %, C4 -1.5 %, 4-way C5
+    // shard -6 %; larger static shares made C4 up to 25 % slower, the whole
+    // share made both slower.
+    const long long first_take = per_warp < 3 ? 0 : DPL == 1 ? per_warp * 3 / 4 : per_warp / 2;
     const int fetch_arg = fetch | (int)(std::min<long long>(first_take, 255) << 8);
     static std::atomic<int> slot{0};
     const int qs = g_queue_slot_override >= 0 ? g_queue_slot_override
