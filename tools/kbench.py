@@ -27,6 +27,17 @@ def main():
     for name, build in (("c5", lambda: bench.build_c5(bench.shard_plan(0, 1), "frontier")),
                         ("c4", lambda: bench.build_c4("sweep"))):
         cfg, bank, states, work = build()
+        if name == "c4" and order == "shuffle":
+            # stages in a fixed pseudo-random order within each scenario
+            import numpy as np
+
+            from paper_2605_07238_b200 import pack
+
+            rng = np.random.default_rng(7)
+            key = rng.permutation(int(work.stage.max()) + 1)[work.stage]
+            idx = np.lexsort((key, work.scen))
+            work = pack.make_work(bank, zip(work.scen[idx].tolist(), work.stage[idx].tolist()),
+                                  cfg.weights.ablation.no_shard)
         if name == "c4" and order == "stage":
             import numpy as np
 
