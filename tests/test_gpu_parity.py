@@ -450,3 +450,28 @@ def test_more_concurrent_launches_than_rotating_counter_slots():
         assert np.array_equal(bits(o.psi.cpu().numpy()[:n]), want)
     for h in raw:
         cudart.cudaStreamDestroy(h)
+
+
+@pytest.mark.parametrize("g", [2, 4, 8])
+def test_strong_scaling_shards_match_oracle(g):
+    """Rank 0's shard at g ranks (bench.shard_plan / bench.c4_plan) scored on
+    the GPU equals the oracle bit for bit.  The shards put the launch in
+    every scheduling regime of the persistent grid: a static first share
+    with multi-item tickets (2-way), a short static share with 2-item
+    tickets (4-way) and single-item tickets (8-way)."""
+    import bench
+
+    cfg, bank, states, work = bench.build_c5(bench.shard_plan(0, g), "frontier")
+    want = oracle.score(bank, pack.weights_record(cfg.weights), states, work,
+                        with_extras=False)["psi"]
+    got = runtime.DeviceBank(bank, cfg.weights).score(states, work, extras=False).psi
+    assert np.array_equal(bits(got.cpu().numpy()[: work.n_psi]), bits(want))
+
+    p = bench.c4_plan(0, g)
+    cfg, bank, states, work = bench.build_c4("sweep", n_scen=p["count"], first_scen=p["first"],
+                                             stage_rank=p["stage_rank"],
+                                             stage_world=p["stage_world"])
+    want = oracle.score(bank, pack.weights_record(cfg.weights), states, work,
+                        with_extras=False)["psi"]
+    got = runtime.DeviceBank(bank, cfg.weights).score(states, work, extras=False).psi
+    assert np.array_equal(bits(got.cpu().numpy()[: work.n_psi]), bits(want))
