@@ -293,12 +293,14 @@ def workload_config(args, world: int) -> dict:
                 "stages_per_instance": 500, "devices": 32, "batch": C5_SHAPE["batch"],
                 "horizon": 3, "scenario_states": "canonical (SURVEY §8(d)), one per instance",
                 "l2": "flushed between steps (256 MiB write, outside the events)",
+                "outputs": "Psi (the FrontierProblem cost matrix), as build_problem",
                 "parallelism": f"dp{world}: contiguous instance ranges of {TOTAL_INSTANCES}"
                                f"/{world} per rank (strong scaling); NCCL all-gather of Psi "
                                "slabs and assignment triples"}
     return {"workload": f"c4_{args.mode}", "instances": 1, "stages_per_instance": 10000,
             "devices": 64, "batch": 16, "horizon": 4, "scenario_states": C4_SCENARIOS,
             "l2": "flushed between steps (256 MiB write, outside the events)",
+            "outputs": "Psi (the FrontierProblem cost matrix), as build_problem",
             "parallelism": f"dp{world}: stages v = rank (mod {world}) of all "
                            f"{C4_SCENARIOS} scenario seeds per rank (strong scaling)"}
 
@@ -728,8 +730,11 @@ def run_fate(args):
     bank_setup_s = time.perf_counter() - t_bank  # once per (bank, weights), not per step
     dstates = dbank.upload_states(states)
     dwork = dbank.upload_work(work)
-    out = dbank.alloc_out(work, extras=True)
-    out.tail = None  # diagnostic only; Psi + S + completion are what FATE consumes
+    # Psi only -- the metric's unit and exactly what the reference's
+    # build_problem / plan_score computes (and what the reference arm and the
+    # e2e pipeline compute); S, tail and completion are the drop-in policy's
+    # extra outputs, timed in c2_fate_runs
+    out = dbank.alloc_out(work, extras=False)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MiB
     torch.cuda.synchronize(device)
 
@@ -813,8 +818,7 @@ def run_fate(args):
         wcfg, wbank, wstates, wwork = build_c5(wplan, args.mode)
         wdb = runtime.DeviceBank(wbank, wcfg.weights, device=device)
         wds, wdw = wdb.upload_states(wstates), wdb.upload_work(wwork)
-        wout = wdb.alloc_out(wwork, extras=True)
-        wout.tail = None
+        wout = wdb.alloc_out(wwork, extras=False)
         wms, _ = time_device(torch, wdb, wds, wdw, wout, args.steps, args.warmup, flush, world,
                              device)
         wmax = reduce_max(wms, world, device)
@@ -1049,8 +1053,7 @@ def measure_c4(torch, device, args, rank: int = 0, world: int = 1) -> dict:
     dbank = runtime.DeviceBank(bank, cfg.weights, device=device)
     dstates = dbank.upload_states(states)
     dwork = dbank.upload_work(work)
-    out = dbank.alloc_out(work, extras=True)
-    out.tail = None
+    out = dbank.alloc_out(work, extras=False)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)
     clocks = ClockSampler(device.index or 0)
     ms, launches = time_device(torch, dbank, dstates, dwork, out, max(5, args.steps // 4),

@@ -48,7 +48,7 @@ def main():
                                   cfg.weights.ablation.no_shard)
         db = runtime.DeviceBank(bank, cfg.weights, device=dev)
         ds, dw = db.upload_states(states), db.upload_work(work)
-        o = db.alloc_out(work, extras=True)
+        o = db.alloc_out(work, extras=not os.environ.get("KB_PSI_ONLY"))
         if not os.environ.get("KB_TAIL"):
             o.tail = None
         if os.environ.get("KB_NO_SCHED"):

@@ -45,8 +45,7 @@ def main():
                                                              stage_world=pl["stage_world"])
                 db = runtime.DeviceBank(bank, cfg.weights, device=dev)
                 ds, dw = db.upload_states(states), db.upload_work(work)
-                o = db.alloc_out(work, extras=True)
-                o.tail = None
+                o = db.alloc_out(work, extras=False)  # Psi only, as bench.py
                 ms = sorted(bench.time_device(torch, db, ds, dw, o, steps, 5, flush, 1, dev)[0]
                             for _ in range(3))[1]
                 per_rank.append((ms, work.n_psi, work.n_items))
